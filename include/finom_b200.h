@@ -1,0 +1,112 @@
+/*
+ * finom_b200.h -- C ABI of the B200-native FINOM hot path.
+ *
+ * The reference (pure Python + numba, /root/reference/pkg/src/finom) has no
+ * native FFI; its hot path is the numba kernel table routed by
+ * _kernels._route (_kernels.py:540-596).  Each entry point below replaces
+ * one of those kernels or the Python loop that drives them; the reference
+ * interface it stands in for is cited per function.  INTEGRATION.md shows
+ * the ctypes binding a maintainer would add to finom._kernels.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; `stream` is a cudaStream_t (NULL = the
+ *     legacy default stream);
+ *   - *_dev pointers are device memory, *_host pointers host memory;
+ *   - every function returns a status: 0 OK, 1 ZERO_DENOM, 2 NONFINITE
+ *     (_kernels.py:47-50), >= 100 argument / CUDA errors
+ *     (finom_last_error() has the message);
+ *   - 1D problems are batched: P problems, problem p owns
+ *     x[xoff[p] .. xoff[p+1]) and y[yoff[p] .. yoff[p+1]) of the
+ *     concatenated meshes (P = 1 is the reference's single problem);
+ *   - no global mutable state: a plan owns its buffers; distinct plans may
+ *     be used from different host threads on different streams.
+ */
+#ifndef FINOM_B200_H
+#define FINOM_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FINOM_OK 0
+#define FINOM_ZERO_DENOM 1
+#define FINOM_NONFINITE 2
+#define FINOM_EARG 100
+#define FINOM_ECUDA 101
+
+typedef struct finom_plan1d finom_plan1d;
+
+/* Message of the last error on this thread. */
+const char *finom_last_error(void);
+
+/* Library / kernel build identification (sm_100a). */
+const char *finom_build_info(void);
+
+/* Builds the device plan for P 1D problems: uploads the meshes, computes the
+ * dividing-index tile partition (kernel1d.dividing_index,
+ * kernel1d.py:55-62, and the merge-path split of x U y) and allocates the
+ * work buffers.  Replaces kernel1d.build_operator (kernel1d.py:234-255):
+ * no kernel tables are stored; every factor is recomputed on the fly. */
+int finom_plan1d_create(int64_t P, const int64_t *xoff_host, const double *x_host,
+                        const int64_t *yoff_host, const double *y_host,
+                        const double *eps_host, void *stream, finom_plan1d **plan_out);
+int finom_plan1d_destroy(finom_plan1d *plan);
+/* Number of tiles, points etc. (for tests and bench accounting). */
+int finom_plan1d_info(const finom_plan1d *plan, int64_t *info8);
+
+/* The scaling loop for every problem of the plan, entirely on device:
+ * solver.run_driver (solver.py:156-199) with adapter.iterate ==
+ * _kernels.iter_1d (_kernels.py:260-350) and adapter.absorb ==
+ * kernel1d.absorb + solver._shift (kernel1d.py:313-325, solver.py:135-153).
+ *   u_dev, v_dev        weights (concatenated like x, y)
+ *   phi_dev, psi_dev    out: scaling vectors (initialised to 1/n inside)
+ *   a_dev, b_dev        out: accumulated log-domain shifts
+ *   hist_dev            out: P x itr_max, err of every iteration
+ *                       (history cadence is applied by the caller)
+ *   info_dev            out: P x 5 int64: iterations_run, converged,
+ *                       status, n_absorb, failed iteration
+ *   absorb_its_dev      out (nullable): P x itr_max absorb iterations
+ * Returns the worst per-problem status (0 if all problems ran clean). */
+int finom_solve1d(finom_plan1d *plan, const double *u_dev, const double *v_dev,
+                  double *phi_dev, double *psi_dev, double *a_dev, double *b_dev,
+                  int64_t itr_max, double tol, int stabilize, double absorb_threshold,
+                  double *hist_dev, int64_t *info_dev, int64_t *absorb_its_dev, void *stream);
+
+/* transport_cost_fast (solver.py:252-271) per problem, with the shifts
+ * a_dev/b_dev (nullable = zero) folded into the kernel. cost_dev: P doubles. */
+int finom_cost1d(finom_plan1d *plan, const double *a_dev, const double *b_dev,
+                 const double *phi_dev, const double *psi_dev, double *cost_dev, void *stream);
+
+/* kernel1d.apply / apply_transpose / apply_blocks (kernel1d.py:284-310),
+ * i.e. _kernels.dp_apply / dp_blocks (_kernels.py:53-125) on the operator
+ * with shifts a_dev/b_dev (nullable = zero).
+ *   mode 0: out = K' in   (in: len m per problem, out: len n)
+ *   mode 1: out = K'^T in (in: len n, out: len m)
+ *   mode 2: out = K'_L in, out2 = K'_U in (blocks of mode 0) */
+int finom_apply1d(finom_plan1d *plan, const double *a_dev, const double *b_dev,
+                  const double *in_dev, int mode, double *out_dev, double *out2_dev,
+                  void *stream);
+
+/* One scaling iteration from an arbitrary state, in place: the adapter
+ * protocol's iterate(u, v, phi, psi) (solver.py:1-16, :126-128) for a
+ * kernel carrying shifts a_dev/b_dev (nullable).  res_dev receives, per
+ * problem, 6 doubles: err, status, psmax, psmin, phmax, phmin. */
+int finom_iterate1d(finom_plan1d *plan, const double *u_dev, const double *v_dev,
+                    double *phi_dev, double *psi_dev, const double *a_dev, const double *b_dev,
+                    double *res_dev, void *stream);
+
+/* End-to-end call with HOST buffers (one problem): sinkhorn_1d
+ * (solver.py:202-230) including transport_cost_fast.  hist_host: itr_max
+ * doubles; info_host: 5 int64 (as finom_solve1d); cost_host: 1 double.
+ * timing_host (nullable): 3 doubles = setup s, loop s, cost s. */
+int finom_sinkhorn1d_host(int64_t n, const double *x, int64_t m, const double *y,
+                          const double *u, const double *v, double eps, int64_t itr_max,
+                          double tol, int stabilize, double absorb_threshold, double *phi,
+                          double *psi, double *a, double *b, double *hist, int64_t *info,
+                          int64_t *absorb_its, double *cost, double *timing_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

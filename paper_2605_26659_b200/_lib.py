@@ -1,0 +1,130 @@
+"""ctypes binding of the C ABI in include/finom_b200.h.
+
+This is the only route to the numerics: there is no CPU fallback and no
+backend switch.  If the shared library is missing or no CUDA device is
+visible, every entry point raises DeviceError.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import DeviceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfinom_b200.so")
+
+_c_i64 = ctypes.c_int64
+_c_dbl = ctypes.c_double
+_c_int = ctypes.c_int
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); must match include/finom_b200.h
+SIGNATURES = {
+    "finom_last_error": (ctypes.c_char_p, []),
+    "finom_build_info": (ctypes.c_char_p, []),
+    "finom_plan1d_create": (_c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_plan1d_destroy": (_c_int, [_vp]),
+    "finom_plan1d_info": (_c_int, [_vp, _vp]),
+    "finom_solve1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int,
+                               _c_dbl, _vp, _vp, _vp, _vp]),
+    "finom_cost1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_apply1d": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _vp, _vp]),
+    "finom_iterate1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_sinkhorn1d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _vp, _vp, _c_dbl, _c_i64,
+                                       _c_dbl, _c_int, _c_dbl, _vp, _vp, _vp, _vp, _vp, _vp,
+                                       _vp, _vp, _vp]),
+}
+
+_lib = None
+
+
+def load(require_device=True):
+    """Load libfinom_b200.so (and check a CUDA device is present)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                "CUDA extension %s is not built; run __graft_entry__.build()" % LIB_PATH)
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_device:
+        import torch
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device visible; the FINOM B200 path has no CPU fallback")
+    return _lib
+
+
+def last_error():
+    return load(False).finom_last_error().decode()
+
+
+def ptr(a):
+    """Raw pointer of a numpy array or a torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def stream_ptr():
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def check(code, what):
+    """Map a C status >= 100 to DeviceError; return FINOM status 0/1/2."""
+    if code >= 100:
+        raise DeviceError("%s failed: %s" % (what, last_error()))
+    return code
+
+
+class Plan1D:
+    """Device plan for a batch of P 1D problems (finom_plan1d_create)."""
+
+    def __init__(self, xs, ys, eps):
+        lib = load()
+        xs = [np.ascontiguousarray(x, dtype=np.float64) for x in xs]
+        ys = [np.ascontiguousarray(y, dtype=np.float64) for y in ys]
+        self.P = len(xs)
+        self.xoff = np.zeros(self.P + 1, dtype=np.int64)
+        self.yoff = np.zeros(self.P + 1, dtype=np.int64)
+        self.xoff[1:] = np.cumsum([x.size for x in xs])
+        self.yoff[1:] = np.cumsum([y.size for y in ys])
+        self.x = np.concatenate(xs) if self.P > 1 else xs[0]
+        self.y = np.concatenate(ys) if self.P > 1 else ys[0]
+        self.eps = np.ascontiguousarray(np.broadcast_to(np.asarray(eps, dtype=np.float64),
+                                                        (self.P,)))
+        h = ctypes.c_void_p()
+        check(lib.finom_plan1d_create(self.P, ptr(self.xoff), ptr(self.x), ptr(self.yoff),
+                                      ptr(self.y), ptr(self.eps), stream_ptr(),
+                                      ctypes.byref(h)), "finom_plan1d_create")
+        self._h = h
+        self._lib = lib
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        out = np.zeros(8, dtype=np.int64)
+        check(self._lib.finom_plan1d_info(self._h, ptr(out)), "finom_plan1d_info")
+        keys = ("P", "tiles", "NX", "NY", "max_tiles", "tile", "threads", "smem")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.finom_plan1d_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

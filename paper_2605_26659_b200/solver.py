@@ -1,0 +1,381 @@
+"""Scaling-iteration driver and the B200 1D solver (drop-in for finom.solver).
+
+Same names, fields, defaults, validation and exceptions as the reference
+(pkg/src/finom/solver.py).  The difference is where the loop runs:
+``sinkhorn_1d`` hands the whole ``run_driver`` loop (solver.py:156-199) to
+the device (finom_solve1d: one CUDA graph per chunk of iterations, with
+history, stopping rule and absorption decided on device), so there is no
+per-iteration host round trip.  ``run_driver`` itself is kept for the
+adapter protocol (solver.py:1-16) and accepts the GPU adapter
+``GpuAdapter1D`` as well as any reference adapter.
+"""
+
+import ctypes
+from dataclasses import dataclass
+from time import perf_counter
+from typing import Optional
+
+import numpy as np
+
+from . import _lib, kernel1d
+from .errors import (
+    ConfigError,
+    DimensionMismatch,
+    InvalidEpsilon,
+    NonFiniteIterate,
+    SizeCapExceeded,
+    ZeroDenominator,
+)
+
+OK, ZERO_DENOM, NONFINITE = 0, 1, 2  # _kernels.py:47-50
+
+_MSG_ZD = ("a matvec underflowed to zero on an entry with positive "
+           "target mass; enable stabilization or increase epsilon")
+_MSG_NF = ("scaling update produced a non-finite value; enable "
+           "stabilization or increase epsilon")
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """solver.py:36-61, same defaults and validation."""
+
+    epsilon: float
+    itr_max: int = 1000
+    tol: float = 1e-9
+    stabilize: bool = False
+    absorb_threshold: float = 200.0
+    check_every: int = 1
+    plan_cap: int = 10**8
+
+    def __post_init__(self):
+        eps = float(self.epsilon)
+        if not np.isfinite(eps) or eps <= 0:
+            raise InvalidEpsilon("epsilon must be a positive finite real")
+        object.__setattr__(self, "epsilon", eps)
+        if self.itr_max < 1:
+            raise ConfigError("itr_max must be at least 1")
+        if not np.isfinite(self.tol) or self.tol < 0:
+            raise ConfigError("tol must be a nonnegative finite real")
+        if not np.isfinite(self.absorb_threshold) or self.absorb_threshold <= 1:
+            raise ConfigError("absorb_threshold must exceed 1")
+        if self.check_every < 1:
+            raise ConfigError("check_every must be at least 1")
+        if self.plan_cap < 1:
+            raise ConfigError("plan_cap must be positive")
+
+
+@dataclass
+class SolverState:
+    """solver.py:64-73."""
+
+    phi: np.ndarray
+    psi: np.ndarray
+    a: Optional[np.ndarray] = None
+    b: Optional[np.ndarray] = None
+    iteration: int = 0
+    last_marginal_error: float = np.inf
+
+
+@dataclass
+class Solution:
+    """solver.py:76-89.  ``kernel`` is a device-backed operator handle."""
+
+    phi: np.ndarray
+    psi: np.ndarray
+    a: np.ndarray
+    b: np.ndarray
+    kernel: object
+    iterations_run: int
+    converged: bool
+    marginal_error_history: list
+    wall_time: float
+    setup_time: float
+    cost: float
+    config: SolverConfig
+    absorb_iterations: Optional[list] = None
+
+
+def raise_status(status):
+    """Status code -> the reference's exception (solver.py:177-184)."""
+    if status == ZERO_DENOM:
+        raise ZeroDenominator(_MSG_ZD)
+    if status == NONFINITE:
+        raise NonFiniteIterate(_MSG_NF)
+
+
+def history_from(errs, iterations, converged, config):
+    """Apply the reference's recording cadence (solver.py:185-192) to per-iteration errors."""
+    hist = []
+    for it in range(1, iterations + 1):
+        if it % config.check_every == 0 or it == config.itr_max:
+            hist.append((it, float(errs[it - 1])))
+    if converged and (not hist or hist[-1][0] != iterations):
+        hist.append((iterations, float(errs[iterations - 1])))
+    return hist
+
+
+def _shift(weights, scaling, epsilon):
+    """solver.py:135-153 (host copy, used by run_driver with reference adapters)."""
+    pos = weights > 0
+    vals = epsilon * np.log(scaling[pos])
+    if pos.all():
+        return vals
+    out = np.empty(weights.shape[0])
+    idx = np.arange(weights.shape[0], dtype=float)
+    out[pos] = vals
+    out[~pos] = np.interp(idx[~pos], idx[pos], vals)
+    return out
+
+
+def run_driver(adapter, u, v, config):
+    """The reference's scaling loop over any adapter (solver.py:156-199)."""
+    n = u.shape[0]
+    phi = np.full(n, 1.0 / n)
+    psi = np.full(v.shape[0], 1.0 / n)
+    hi_cut = np.exp(config.absorb_threshold)
+    lo_cut = np.exp(-config.absorb_threshold)
+    history = []
+    converged = False
+    it = 0
+    t0 = perf_counter()
+    while it < config.itr_max:
+        err, status, psmax, psmin, phmax, phmin = adapter.iterate(u, v, phi, psi)
+        it += 1
+        raise_status(status)
+        recorded = it % config.check_every == 0 or it == config.itr_max
+        if recorded:
+            history.append((it, float(err)))
+        if config.tol > 0 and err <= config.tol:
+            if not recorded:
+                history.append((it, float(err)))
+            converged = True
+            break
+        if config.stabilize and (phmax > hi_cut or psmax > hi_cut
+                                 or phmin < lo_cut or psmin < lo_cut):
+            adapter.absorb(_shift(u, phi, config.epsilon), _shift(v, psi, config.epsilon))
+            phi[:] = 1.0
+            psi[:] = 1.0
+    return phi, psi, it, converged, history, perf_counter() - t0
+
+
+class GpuAdapter1D:
+    """Adapter-protocol backend on the B200 kernels (solver.py:1-16, :92-132).
+
+    ``iterate`` runs one fused iteration on device (finom_iterate1d) and
+    updates phi/psi in place, so the reference's own run_driver can drive it.
+    """
+
+    def __init__(self, x, y, epsilon):
+        self.op = kernel1d.build_operator(x, y, epsilon)
+
+    @property
+    def kernel(self):
+        return self.op
+
+    @property
+    def a(self):
+        return self.op.absorption_left
+
+    @property
+    def b(self):
+        return self.op.absorption_right
+
+    def iterate(self, u, v, phi, psi):
+        import torch
+        dev = torch.device("cuda")
+        plan = self.op.plan()
+        tu = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)).to(dev)
+        tv = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
+        tphi = torch.from_numpy(np.ascontiguousarray(phi)).to(dev)
+        tpsi = torch.from_numpy(np.ascontiguousarray(psi)).to(dev)
+        ta = tb = None
+        if self.op.absorbed:
+            ta = torch.from_numpy(np.ascontiguousarray(self.a)).to(dev)
+            tb = torch.from_numpy(np.ascontiguousarray(self.b)).to(dev)
+        res = torch.zeros(6, dtype=torch.float64, device=dev)
+        lib = _lib.load()
+        _lib.check(lib.finom_iterate1d(plan.handle, _lib.ptr(tu), _lib.ptr(tv), _lib.ptr(tphi),
+                                       _lib.ptr(tpsi), _lib.ptr(ta), _lib.ptr(tb), _lib.ptr(res),
+                                       _lib.stream_ptr()), "finom_iterate1d")
+        r = res.cpu().numpy()
+        phi[:] = tphi.cpu().numpy()
+        psi[:] = tpsi.cpu().numpy()
+        return float(r[0]), int(r[1]), float(r[2]), float(r[3]), float(r[4]), float(r[5])
+
+    def absorb(self, delta_a, delta_b):
+        self.op = kernel1d.absorb(self.op, delta_a, delta_b)
+
+
+def sinkhorn_1d(x, y, u, v, config):
+    """Entropic scaling on 1D meshes, whole loop on the B200 (solver.py:202-230)."""
+    if len(u.weights) != len(x):
+        raise DimensionMismatch("u must have one weight per source node")
+    if len(v.weights) != len(y):
+        raise DimensionMismatch("v must have one weight per target node")
+    lib = _lib.load()
+    n, m, itr = len(x), len(y), int(config.itr_max)
+    phi, a = np.empty(n), np.empty(n)
+    psi, b = np.empty(m), np.empty(m)
+    hist = np.zeros(itr)
+    info = np.zeros(5, dtype=np.int64)
+    abs_its = np.zeros(itr, dtype=np.int64)
+    cost = np.zeros(1)
+    timing = np.zeros(3)
+    status = _lib.check(lib.finom_sinkhorn1d_host(
+        n, _lib.ptr(x.nodes), m, _lib.ptr(y.nodes), _lib.ptr(u.weights), _lib.ptr(v.weights),
+        config.epsilon, itr, float(config.tol), int(bool(config.stabilize)),
+        float(config.absorb_threshold), _lib.ptr(phi), _lib.ptr(psi), _lib.ptr(a), _lib.ptr(b),
+        _lib.ptr(hist), _lib.ptr(info), _lib.ptr(abs_its), _lib.ptr(cost), _lib.ptr(timing)),
+        "finom_sinkhorn1d_host")
+    raise_status(status)
+    its, conv = int(info[0]), bool(info[1])
+    op = kernel1d.build_operator(x, y, config.epsilon)
+    op = kernel1d.KernelOperator1D(x, y, op.epsilon, a, b, op._plans)
+    return Solution(
+        phi=phi, psi=psi, a=a, b=b, kernel=op, iterations_run=its, converged=conv,
+        marginal_error_history=history_from(hist, its, conv, config),
+        wall_time=float(timing[0] + timing[1]), setup_time=float(timing[0]),
+        cost=float(cost[0]), config=config,
+        absorb_iterations=[int(k) for k in abs_its[:int(info[3])]])
+
+
+class BatchSolver1D:
+    """Device-resident batch of independent 1D problems (no reference equivalent;
+    per-problem semantics == sinkhorn_1d).  Inputs stay in HBM between solves."""
+
+    def __init__(self, xs, ys, us, vs, epsilons):
+        import torch
+        if not (len(xs) == len(ys) == len(us) == len(vs)):
+            raise DimensionMismatch("xs, ys, us, vs must have one entry per problem")
+        for k, (x, y, u, v) in enumerate(zip(xs, ys, us, vs)):
+            if len(u) != len(x) or len(v) != len(y):
+                raise DimensionMismatch("problem %d: weight/mesh length mismatch" % k)
+        eps = np.broadcast_to(np.asarray(epsilons, dtype=np.float64), (len(xs),))
+        for e in eps:
+            if not np.isfinite(e) or e <= 0:
+                raise InvalidEpsilon("epsilon must be a positive finite real")
+        node = lambda z: z.nodes if hasattr(z, "nodes") else np.asarray(z, dtype=np.float64)
+        wts = lambda z: z.weights if hasattr(z, "weights") else np.asarray(z, dtype=np.float64)
+        self.plan = _lib.Plan1D([node(x) for x in xs], [node(y) for y in ys], eps)
+        dev = torch.device("cuda")
+        self.P = self.plan.P
+        self.eps = np.array(eps)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.u = torch.from_numpy(np.concatenate([wts(u) for u in us])).to(dev)
+        self.v = torch.from_numpy(np.concatenate([wts(v) for v in vs])).to(dev)
+        NX, NY = self.u.numel(), self.v.numel()
+        self.phi = torch.empty(NX, **f64)
+        self.psi = torch.empty(NY, **f64)
+        self.a = torch.empty(NX, **f64)
+        self.b = torch.empty(NY, **f64)
+        self.cost = torch.empty(self.P, **f64)
+        self._itr = None
+
+    def _bufs(self, itr):
+        import torch
+        if self._itr != itr:
+            dev = self.phi.device
+            self.hist = torch.zeros(self.P * itr, dtype=torch.float64, device=dev)
+            self.info = torch.zeros(self.P * 5, dtype=torch.int64, device=dev)
+            self.abs_its = torch.zeros(self.P * itr, dtype=torch.int64, device=dev)
+            self._itr = itr
+
+    def solve(self, itr_max, tol=0.0, stabilize=True, absorb_threshold=200.0):
+        """Run the device loop; returns the worst status (0/1/2). No host sync inside."""
+        self._bufs(int(itr_max))
+        lib = _lib.load()
+        return _lib.check(lib.finom_solve1d(
+            self.plan.handle, _lib.ptr(self.u), _lib.ptr(self.v), _lib.ptr(self.phi),
+            _lib.ptr(self.psi), _lib.ptr(self.a), _lib.ptr(self.b), int(itr_max), float(tol),
+            int(bool(stabilize)), float(absorb_threshold), _lib.ptr(self.hist),
+            _lib.ptr(self.info), _lib.ptr(self.abs_its), _lib.stream_ptr()), "finom_solve1d")
+
+    def compute_cost(self):
+        lib = _lib.load()
+        _lib.check(lib.finom_cost1d(self.plan.handle, _lib.ptr(self.a), _lib.ptr(self.b),
+                                    _lib.ptr(self.phi), _lib.ptr(self.psi),
+                                    _lib.ptr(self.cost), _lib.stream_ptr()), "finom_cost1d")
+        return self.cost
+
+
+def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
+    """Batch of independent sinkhorn_1d problems in one device loop.
+
+    ``config`` supplies itr_max / tol / stabilize / threshold / cadence for all
+    problems; ``epsilons`` (optional) overrides config.epsilon per problem.
+    Raises the reference's exception if any problem fails.
+    """
+    eps = config.epsilon if epsilons is None else epsilons
+    t0 = perf_counter()
+    bs = BatchSolver1D(xs, ys, us, vs, eps)
+    setup = perf_counter() - t0
+    t1 = perf_counter()
+    status = bs.solve(config.itr_max, config.tol, config.stabilize, config.absorb_threshold)
+    info = bs.info.view(bs.P, 5).cpu().numpy()
+    loop = perf_counter() - t1
+    raise_status(status)
+    bs.compute_cost()
+    hist = bs.hist.view(bs.P, -1).cpu().numpy()
+    abs_its = bs.abs_its.view(bs.P, -1).cpu().numpy()
+    cost = bs.cost.cpu().numpy()
+    phi, psi = bs.phi.cpu().numpy(), bs.psi.cpu().numpy()
+    a, b = bs.a.cpu().numpy(), bs.b.cpu().numpy()
+    xo, yo = bs.plan.xoff, bs.plan.yoff
+    sols = []
+    for p in range(bs.P):
+        x = xs[p] if hasattr(xs[p], "nodes") else None
+        y = ys[p] if hasattr(ys[p], "nodes") else None
+        sl, tl = slice(xo[p], xo[p + 1]), slice(yo[p], yo[p + 1])
+        cfg = SolverConfig(epsilon=float(bs.eps[p]), itr_max=config.itr_max, tol=config.tol,
+                           stabilize=config.stabilize, absorb_threshold=config.absorb_threshold,
+                           check_every=config.check_every, plan_cap=config.plan_cap)
+        op = None
+        if x is not None and y is not None:
+            op0 = kernel1d.build_operator(x, y, cfg.epsilon)
+            op = kernel1d.KernelOperator1D(x, y, op0.epsilon, a[sl].copy(), b[tl].copy(),
+                                           op0._plans)
+        its, conv = int(info[p, 0]), bool(info[p, 1])
+        sols.append(Solution(
+            phi=phi[sl].copy(), psi=psi[tl].copy(), a=a[sl].copy(), b=b[tl].copy(), kernel=op,
+            iterations_run=its, converged=conv,
+            marginal_error_history=history_from(hist[p], its, conv, cfg),
+            wall_time=setup + loop, setup_time=setup, cost=float(cost[p]), config=cfg,
+            absorb_iterations=[int(k) for k in abs_its[p, :int(info[p, 3])]]))
+    return sols
+
+
+def marginal_error(state, kernel, v):
+    """L1 distance of diag(psi) K^T phi from the target weights (solver.py:233-237)."""
+    w = v.weights if hasattr(v, "weights") else np.asarray(v, dtype=float)
+    t = kernel.apply_transpose(state.phi)
+    return float(np.sum(np.abs(state.psi * t - w)))
+
+
+def plan_dense(solution):
+    """diag(phi) K diag(psi) (solver.py:240-249)."""
+    kern = solution.kernel
+    n, m = kern.shape
+    if n * m > solution.config.plan_cap:
+        raise SizeCapExceeded("plan has %d entries, cap is %d" % (n * m, solution.config.plan_cap))
+    dense = kern.dense_realization()
+    return solution.phi[:, None] * dense * solution.psi[None, :]
+
+
+def transport_cost_fast(solution):
+    """<C, plan> in linear time on the device (solver.py:252-271)."""
+    import torch
+    op = solution.kernel
+    if not isinstance(op, kernel1d.KernelOperator1D):
+        from .kernel2d import transport_cost_fast_2d
+        return transport_cost_fast_2d(solution)
+    dev = torch.device("cuda")
+    plan = op.plan()
+    t = lambda arr: torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(dev)
+    tphi, tpsi = t(solution.phi), t(solution.psi)
+    ta = t(op.absorption_left) if op.absorbed else None
+    tb = t(op.absorption_right) if op.absorbed else None
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.finom_cost1d(plan.handle, _lib.ptr(ta), _lib.ptr(tb), _lib.ptr(tphi),
+                                _lib.ptr(tpsi), _lib.ptr(out), _lib.stream_ptr()), "finom_cost1d")
+    return float(out.item())

@@ -1,0 +1,225 @@
+"""Generate the golden fixtures in tests/golden from the REFERENCE package.
+
+Run in the build container (the reference is not available on the GPU box):
+    python tests/golden/make_golden.py
+It imports /root/reference/pkg/src/finom (read-only; numba cache redirected)
+and records the reference's own outputs on seeded inputs.  The fixtures pin
+both the C oracle (tests/test_oracle.py, CPU) and the CUDA path
+(tests/test_parity_gpu.py).
+"""
+
+import json
+import os
+import sys
+import time
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_finom_golden")
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+
+import numpy as np  # noqa: E402
+from finom import kernel1d as rk  # noqa: E402
+from finom import mesh as rm  # noqa: E402
+from finom import solver as rs  # noqa: E402
+from finom import kernel2d as r2  # noqa: E402
+
+from paper_2605_26659_b200 import workloads as W  # noqa: E402
+
+
+class CountingAdapter(rs._FastAdapter1D):
+    """The reference adapter, recording the iterations at which it absorbs."""
+
+    def __init__(self, *a):
+        super().__init__(*a)
+        self.calls = 0
+        self.absorbs = []
+
+    def iterate(self, *a):
+        self.calls += 1
+        return super().iterate(*a)
+
+    def absorb(self, da, db):
+        self.absorbs.append(self.calls)
+        super().absorb(da, db)
+
+
+def ref_solve(x, y, u, v, cfg):
+    """sinkhorn_1d (solver.py:202-230) with absorb iterations recorded."""
+    X, Y, Um, Vm = rm.Mesh1D(x), rm.Mesh1D(y), rm.Measure(u), rm.Measure(v)
+    ad = CountingAdapter(X, Y, cfg.epsilon)
+    phi, psi, it, conv, hist, loop = rs.run_driver(ad, Um.weights, Vm.weights, cfg)
+    sol = rs.Solution(phi=phi, psi=psi, a=ad.a, b=ad.b, kernel=ad.kernel, iterations_run=it,
+                      converged=conv, marginal_error_history=hist, wall_time=loop,
+                      setup_time=0.0, cost=np.nan, config=cfg)
+    sol.cost = rs.transport_cost_fast(sol)
+    return dict(phi=phi, psi=psi, a=np.asarray(ad.a), b=np.asarray(ad.b),
+                hist_it=np.array([h[0] for h in hist], dtype=np.int64),
+                hist_err=np.array([h[1] for h in hist]), iterations=it, converged=conv,
+                absorb_its=np.array(ad.absorbs, dtype=np.int64), cost=sol.cost, loop_s=loop)
+
+
+def save(name, **arrs):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrs)
+    print("wrote", path, os.path.getsize(path), "bytes")
+
+
+def kernel_cases():
+    """Matvec instances mirroring test_kernel1d.py:261-390 (random, rectangular, shifted)."""
+    rng = np.random.default_rng(5)
+    out = {}
+    GX = np.array([1.0, 3.0, 7.0, 9.0, 12.0])
+    GY = np.array([2.0, 5.0, 6.0, 9.0, 10.0])
+    cases = [(GX, GY, 1.0, None, None)]
+    for k in range(40):
+        n = int(rng.integers(1, 40)) if k % 7 else 1
+        m = int(rng.integers(1, 40)) if k % 5 else 1
+        x = rm.random_sorted_nodes(n, seed=int(rng.integers(2**31))).nodes
+        y = rm.random_sorted_nodes(m, seed=int(rng.integers(2**31))).nodes
+        if k % 9 == 3:  # shared nodes: every node a tie
+            y = x.copy()
+        eps = float(rng.choice([0.01, 0.1, 1.0]))
+        a = b = None
+        if k % 3 == 1:
+            a = rng.normal(0.0, 0.5, n) * eps * 10
+            b = rng.normal(0.0, 0.5, m) * eps * 10
+        cases.append((x, y, eps, a, b))
+    # large-shift rebuild case (test_kernel1d.py:379-390)
+    cases.append((GX, GY, 0.01, np.full(5, 8.0), np.full(5, -8.0)))
+    for k, (x, y, eps, a, b) in enumerate(cases):
+        op = rk.build_operator(rm.Mesh1D(x), rm.Mesh1D(y), eps)
+        if a is not None:
+            op = op.absorb(a, b)
+        psi = rng.random(len(y))
+        phi = rng.random(len(x))
+        p, q = rk.apply_blocks(op, psi)
+        out["c%d_x" % k] = x
+        out["c%d_y" % k] = y
+        out["c%d_eps" % k] = np.array(eps)
+        out["c%d_a" % k] = np.asarray(op.absorption_left)
+        out["c%d_b" % k] = np.asarray(op.absorption_right)
+        out["c%d_psi" % k] = psi
+        out["c%d_phi" % k] = phi
+        out["c%d_Kpsi" % k] = op.apply(psi)
+        out["c%d_KTphi" % k] = op.apply_transpose(phi)
+        out["c%d_p" % k] = p
+        out["c%d_q" % k] = q
+    out["ncases"] = np.array(len(cases))
+    save("kernel1d_cases.npz", **out)
+
+
+def solver_cases():
+    """Small scaling runs mirroring test_solver.py (plain, stabilized, zero mass, rect)."""
+    out = {}
+    cases = []
+    def rp(n, m, seed):
+        return (rm.random_sorted_nodes(n, seed).nodes, rm.random_sorted_nodes(m, seed + 1000).nodes,
+                rm.random_measure(n, seed + 2000).weights, rm.random_measure(m, seed + 3000).weights)
+    cases.append(rp(40, 55, 3) + (rs.SolverConfig(epsilon=0.05, itr_max=800, tol=0.0),))
+    cases.append(rp(40, 55, 3) + (rs.SolverConfig(epsilon=0.05, itr_max=800, tol=0.0, stabilize=True,
+                                                  absorb_threshold=1.5),))
+    cases.append(rp(40, 55, 3) + (rs.SolverConfig(epsilon=0.05, itr_max=20000, tol=1e-11,
+                                                  stabilize=True, absorb_threshold=1.5),))
+    cases.append(rp(30, 30, 4) + (rs.SolverConfig(epsilon=0.01, itr_max=20, tol=0.0, check_every=7),))
+    cases.append(rp(64, 64, 14) + (rs.SolverConfig(epsilon=0.1, itr_max=20000, tol=1e-10),))
+    cases.append(rp(35, 70, 15) + (rs.SolverConfig(epsilon=0.02, itr_max=20000, tol=1e-10,
+                                                   check_every=10),))
+    # zero-mass stretch with absorption (test_solver.py:339-361)
+    x = rm.random_sorted_nodes(80, seed=21).nodes
+    y = rm.random_sorted_nodes(90, seed=22).nodes
+    uw = np.abs(np.random.default_rng(5).normal(size=80))
+    uw[30:45] = 0.0
+    uw[:3] = 0.0
+    cases.append((x, y, uw / uw.sum(), rm.random_measure(90, seed=23).weights,
+                  rs.SolverConfig(epsilon=0.02, itr_max=4000, tol=1e-11, stabilize=True,
+                                  absorb_threshold=1.2)))
+    # eps = 1e-3 rescue (test_solver.py:321-337)
+    x = rm.random_sorted_nodes(300, seed=7).nodes
+    y = rm.random_sorted_nodes(300, seed=8).nodes
+    gm = lambda z, c, w2: np.exp(-(z - c) ** 2 / w2) / np.exp(-(z - c) ** 2 / w2).sum()
+    cases.append((x, y, gm(x, 0.3, 0.001), gm(y, 0.7, 0.001),
+                  rs.SolverConfig(epsilon=0.001, itr_max=2000, tol=0.0, stabilize=True)))
+    # self transport on shared nodes (every node a tie)
+    x = rm.chebyshev_nodes(60).nodes
+    u = rm.random_measure(60, seed=1).weights
+    cases.append((x, x.copy(), u, u.copy(), rs.SolverConfig(epsilon=0.05, itr_max=3000, tol=1e-10)))
+    # single points and degenerate sizes
+    cases.append((np.array([0.2]), np.array([0.9]), np.array([1.0]), np.array([1.0]),
+                  rs.SolverConfig(epsilon=0.7, itr_max=5, tol=0.0)))
+    cases.append((np.array([0.1, 0.4]), np.array([0.25]), np.array([0.3, 0.7]), np.array([1.0]),
+                  rs.SolverConfig(epsilon=0.5, itr_max=50, tol=0.0, stabilize=True,
+                                  absorb_threshold=1.1)))
+    for k, (x, y, u, v, cfg) in enumerate(cases):
+        r = ref_solve(x, y, u, v, cfg)
+        for key in ("x", "y", "u", "v"):
+            out["s%d_%s" % (k, key)] = locals()[key]
+        out["s%d_cfg" % k] = np.array([cfg.epsilon, cfg.itr_max, cfg.tol, float(cfg.stabilize),
+                                       cfg.absorb_threshold, cfg.check_every])
+        for key, val in r.items():
+            out["s%d_%s" % (k, key)] = np.asarray(val)
+    out["ncases"] = np.array(len(cases))
+    save("solver_cases.npz", **out)
+
+
+def failure_cases():
+    """ZeroDenominator / NonFiniteIterate instances (test_solver.py:475-497)."""
+    res = {}
+    for name, (x, y, u, v, eps) in {
+        "zero_denom": ([0.0, 0.5], [0.0, 50.0], [0.5, 0.5], [0.5, 0.5], 0.01),
+        "nonfinite": ([0.0], [713.0], [1.0], [1.0], 1.0),
+    }.items():
+        try:
+            rs.sinkhorn_1d(rm.Mesh1D(x), rm.Mesh1D(y), rm.Measure(u), rm.Measure(v),
+                           rs.SolverConfig(epsilon=eps, itr_max=10, tol=0.0))
+            res[name] = dict(raised=None)
+        except Exception as e:  # noqa: BLE001
+            res[name] = dict(raised=type(e).__name__, message=str(e), x=x, y=y, u=u, v=v, eps=eps)
+    with open(os.path.join(HERE, "failure_cases.json"), "w") as f:
+        json.dump(res, f, indent=1)
+
+
+def config_runs():
+    x, y, u, v, eps = W.config1()
+    r = ref_solve(x, y, u, v, rs.SolverConfig(epsilon=eps, itr_max=500, tol=0.0, stabilize=True))
+    save("config1.npz", **{k: np.asarray(val) for k, val in r.items()})
+    x, y, u, v, eps = W.config2(n=1 << 16)
+    r = ref_solve(x, y, u, v, rs.SolverConfig(epsilon=eps, itr_max=200, tol=0.0, stabilize=True))
+    save("config2_n65536.npz", **{k: np.asarray(val) for k, val in r.items()})
+    probs = {}
+    for p in (0, 1, 2, 3):
+        x, y, u, v, eps = W.config5_problem(p)
+        r = ref_solve(x, y, u, v, rs.SolverConfig(epsilon=eps, itr_max=200, tol=0.0,
+                                                  stabilize=True))
+        for key, val in r.items():
+            probs["p%d_%s" % (p, key)] = np.asarray(val)
+        probs["p%d_eps" % p] = np.array(eps)
+    save("config5_p0-3.npz", **probs)
+
+
+def config2_full():
+    """Full-size config 2 pins: scalars, history and a strided sample of the vectors."""
+    x, y, u, v, eps = W.config2()
+    t = time.time()
+    r = ref_solve(x, y, u, v, rs.SolverConfig(epsilon=eps, itr_max=200, tol=0.0, stabilize=True))
+    dt = time.time() - t
+    stride = 4096
+    save("config2_full_pins.npz", cost=np.array(r["cost"]), hist_err=r["hist_err"],
+         absorb_its=r["absorb_its"], iterations=np.array(r["iterations"]), stride=np.array(stride),
+         phi_s=r["phi"][::stride], psi_s=r["psi"][::stride], a_s=r["a"][::stride],
+         b_s=r["b"][::stride], loop_s=np.array(r["loop_s"]), ref_wall_s=np.array(dt))
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["kernel", "solver", "failure", "configs", "config2_full"]
+    if "kernel" in which:
+        kernel_cases()
+    if "solver" in which:
+        solver_cases()
+    if "failure" in which:
+        failure_cases()
+    if "configs" in which:
+        config_runs()
+    if "config2_full" in which:
+        config2_full()
