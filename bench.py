@@ -1,0 +1,341 @@
+"""Benchmark of the FINOM Sinkhorn hot path on B200 (driver contract).
+
+Default workload: BASELINE.json configs[1] (config 2): 1D W1 Sinkhorn, fp64,
+N = M = 2^22 graded meshes, eps = 1e-3, 200 fixed iterations, log-domain
+stabilization on (absorptions happen inside the timed loop).  One step =
+one full 200-iteration solve through the device-resident loop.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 1|2|5]
+
+value: mesh-points x iterations / s over the device loop, inputs resident
+in HBM (CUDA events on the launching stream, barrier + sync both sides, max
+over ranks).  e2e: the same metric through the public API with host
+buffers (solver.sinkhorn_1d), every copy inside the timed region.
+--impl reference: the reference algorithm on the host CPU (the C oracle
+port, oracle/finom_oracle.c), a bounded sample of the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Sinkhorn mesh-points x iterations/s (fp64)"
+UNIT = "pts*it/s"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(name):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(name, {}).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def workload(cfg, rank=0, world=1):
+    from paper_2605_26659_b200 import workloads as W
+    if cfg == 1:
+        x, y, u, v, eps = W.config1()
+        return dict(xs=[x], ys=[y], us=[u], vs=[v], eps=[eps], itr=500, name="config1")
+    if cfg == 2:
+        x, y, u, v, eps = W.config2()
+        return dict(xs=[x], ys=[y], us=[u], vs=[v], eps=[eps], itr=200, name="config2")
+    if cfg == 5:
+        B = int(os.environ.get("FINOM_BATCH", "8192"))
+        lo, hi = rank * B // world, (rank + 1) * B // world
+        probs = W.config5(batch=B, problems=range(lo, hi))
+        return dict(xs=[p[0] for p in probs], ys=[p[1] for p in probs],
+                    us=[p[2] for p in probs], vs=[p[3] for p in probs],
+                    eps=[p[4] for p in probs], itr=200, name="config5", batch=B)
+    raise SystemExit("unknown config %r" % cfg)
+
+
+def config_json(cfg, wl, world):
+    base = {"l2": "inputs larger than L2 (working set > 126 MB per iteration)",
+            "tol": 0.0, "stabilize": True, "absorb_threshold": 200.0}
+    if cfg == 1:
+        base.update(workload="config1: 1D N=M=1e4 random gaps U[0.2,1.8], eps=1e-2, 500 it",
+                    n=10_000, m=10_000, itr_max=500,
+                    l2="working set 0.9 MB is L2/SM-resident (latency-bound config)")
+    elif cfg == 2:
+        base.update(workload="config2: 1D N=M=2^22 graded meshes x=(i/N)^2, y=1-(1-j/N)^2, "
+                             "3-component mixtures, eps=1e-3, 200 it", n=1 << 22, m=1 << 22,
+                    itr_max=200)
+    else:
+        base.update(workload="config5: batch of %d 1D problems, N=M=16384, eps=10^U[-3,-1], "
+                             "200 it, sharded by problem" % wl["batch"], n=16_384, m=16_384,
+                    batch=wl["batch"], itr_max=200)
+    base["parallelism"] = ("replicas" if cfg != 5 else "problem-sharded") + " x%d" % world
+    return base
+
+
+def run_reference(args):
+    """Reference arm: the reference algorithm (C port of pkg/src/finom) on host CPU."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cfg = args.config
+    wl = workload(cfg) if cfg != 5 else None
+    if cfg == 5:
+        from paper_2605_26659_b200 import workloads as W
+        probs = W.config5(problems=range(4))
+        sample_its = 200
+    else:
+        sample_its = {1: 500, 2: 20}[cfg]
+    vals, loops = [], []
+    for s in range(args.warmup + args.steps):
+        if cfg == 5:
+            t = 0.0
+            pts = 0
+            for p in probs:
+                r = O.sinkhorn_1d(p[0], p[1], p[2], p[3], p[4], sample_its, 0.0, True)
+                t += r["loop_s"]
+                pts += p[0].size
+        else:
+            r = O.sinkhorn_1d(wl["xs"][0], wl["ys"][0], wl["us"][0], wl["vs"][0], wl["eps"][0],
+                              sample_its, 0.0, True)
+            t = r["loop_s"]
+            pts = wl["xs"][0].size
+        if s >= args.warmup:
+            vals.append(pts * sample_its / t)
+            loops.append(t)
+    value = float(statistics.median(vals))
+    sample = ("%s, %d iterations of the full-size problem (stabilize=True), loop window "
+              "(wall_time - setup_time) per step" % ({1: "config1", 2: "config2"}.get(cfg, ""),
+                                                     sample_its)) if cfg != 5 else (
+        "config5 problems 0-3 (of 8192), 200 iterations each, sequential")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(loops),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": config_json(cfg, {"batch": 8192}, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 5])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2605_26659_b200 as fb
+    from paper_2605_26659_b200 import _lib
+
+    cfg = args.config
+    wl = workload(cfg, rank, world)
+    itr = wl["itr"]
+    bs = fb.BatchSolver1D(wl["xs"], wl["ys"], wl["us"], wl["vs"], wl["eps"])
+    pts = int(sum(x.size for x in wl["xs"]))
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else 3):
+        st = bs.solve(itr, 0.0, True, 200.0)
+    torch.cuda.synchronize()
+    if st != 0:
+        raise SystemExit("solve failed with status %d" % st)
+
+    clocks = Clocks(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        bs.solve(itr, 0.0, True, 200.0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    ck = clocks.stop()
+    info = bs.info.view(bs.P, 5).cpu().numpy()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+        tot = torch.tensor([pts], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tot)
+        pts_all = int(tot.item())
+    else:
+        pts_all = pts
+    ms_max = float(ms_t.item())
+    value = pts_all * itr * args.steps / (ms_max * 1e-3)
+
+    # per-kernel timing (events around each launch) for the roofline
+    lib = _lib.load()
+    prof = np.zeros(6)
+    hist_dev = torch.zeros(bs.P * itr, dtype=torch.float64, device="cuda")
+    _lib.check(lib.finom_profile1d(bs.plan.handle, _lib.ptr(bs.u), _lib.ptr(bs.v),
+                                   _lib.ptr(bs.phi), _lib.ptr(bs.psi), _lib.ptr(bs.a),
+                                   _lib.ptr(bs.b), itr, 1, 200.0, _lib.ptr(hist_dev),
+                                   _lib.ptr(prof), _lib.stream_ptr()), "finom_profile1d")
+    NX, NY = bs.u.numel(), bs.v.numel()
+    bytes_a = 8 * (4 * NY + 2 * NX)   # y, v, psi_old, psi_new | x, phi
+    bytes_b = 8 * (3 * NX + 2 * NY)   # x, u, phi_new | y, psi
+    t_half = (prof[0] + prof[1]) * 1e-3
+    achieved = (bytes_a + bytes_b) / t_half / 1e9
+    peak, peak_src = peaks()
+    launches = int(lib.finom_solve1d_launches(bs.plan.handle, itr, 1)) * args.steps
+
+    e2e = None
+    if rank == 0 and cfg != 5:
+        # public API with host buffers: plan + H2D + loop + cost + D2H every step
+        X, Y, U, V = (fb.Mesh1D(wl["xs"][0]), fb.Mesh1D(wl["ys"][0]), fb.Measure(wl["us"][0]),
+                      fb.Measure(wl["vs"][0]))
+        scfg = fb.SolverConfig(epsilon=wl["eps"][0], itr_max=itr, tol=0.0, stabilize=True)
+        fb.sinkhorn_1d(X, Y, U, V, scfg)
+        t0 = time.perf_counter()
+        n_e2e = max(1, min(args.steps, 3))
+        for _ in range(n_e2e):
+            sol = fb.sinkhorn_1d(X, Y, U, V, scfg)
+        dt = (time.perf_counter() - t0) / n_e2e
+        e2e = {"value": pts * itr / dt, "unit": UNIT,
+               "h2d_bytes_per_step": 8 * 2 * (NX + NY), "d2h_bytes_per_step":
+               8 * (2 * NX + 2 * NY + itr + 5 + 1), "cost": sol.cost,
+               "path": "paper_2605_26659_b200.sinkhorn_1d (host numpy in/out, incl. W1 cost)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        if cfg == 5:
+            p = [wl["xs"][0], wl["ys"][0], wl["us"][0], wl["vs"][0], wl["eps"][0]]
+            r = O.sinkhorn_1d(*p, 200, 0.0, True)
+            cpu = {"value": p[0].size * 200 / r["loop_s"], "unit": UNIT, "cores": 1,
+                   "kind": "port", "sample": "config5 problem 0, 200 iterations"}
+        else:
+            its = {1: 500, 2: 60}[cfg]
+            r = O.sinkhorn_1d(wl["xs"][0], wl["ys"][0], wl["us"][0], wl["vs"][0], wl["eps"][0],
+                              its, 0.0, True)
+            cpu = {"value": pts * its / r["loop_s"], "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": "%s full size, first %d of %d iterations (stabilize=True), loop "
+                             "window" % (wl["name"], its, itr)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, BASELINE.json shapes; see DESIGN.md)",
+            "config": config_json(cfg, wl, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic("k_half"),
+                         "peak_source": peak_src,
+                         "kernel": "k_half<A>+k_half<B> (88 B/pt-iteration algorithmic)",
+                         "ms_half_a": prof[0], "ms_half_b": prof[1], "ms_scan": prof[2],
+                         "ms_absorb": prof[3], "ms_iteration_ungraphed": prof[4]},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": ck,
+            "iterations_run": int(info[0, 0]), "absorbs": int(info[0, 3]),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -96,6 +96,18 @@ int finom_iterate1d(finom_plan1d *plan, const double *u_dev, const double *v_dev
                     double *phi_dev, double *psi_dev, const double *a_dev, const double *b_dev,
                     double *res_dev, void *stream);
 
+/* Per-kernel timing of `iters` solve-loop iterations launched without a
+ * graph, CUDA events on `stream` around every launch (bench.py roofline).
+ * ms_out[6]: mean ms of the half-A tile kernel, the half-B tile kernel, one
+ * carry scan, the absorb kernel, one whole iteration; launches/iteration. */
+int finom_profile1d(finom_plan1d *plan, const double *u_dev, const double *v_dev,
+                    double *phi_dev, double *psi_dev, double *a_dev, double *b_dev,
+                    int64_t iters, int stabilize, double absorb_threshold, double *hist_dev,
+                    double *ms_out, void *stream);
+
+/* Number of kernel launches one finom_solve1d call issues. */
+int64_t finom_solve1d_launches(const finom_plan1d *plan, int64_t itr_max, int stabilize);
+
 /* End-to-end call with HOST buffers (one problem): sinkhorn_1d
  * (solver.py:202-230) including transport_cost_fast.  hist_host: itr_max
  * doubles; info_host: 5 int64 (as finom_solve1d); cost_host: 1 double.

@@ -32,8 +32,10 @@
  * in the last ulp on rare arguments; the golden fixtures in
  * tests/golden pin the agreement that results (see tests/test_oracle.py).
  */
+#define _POSIX_C_SOURCE 199309L
 #include <math.h>
 #include <stdint.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -415,12 +417,36 @@ static int ad1_absorb(void *p, const double *da, const double *db) {
     return op1_assemble(&ad->op, ad->x, ad->n, ad->y, ad->m, ad->eps, ad->a, ad->b);
 }
 
+static double now_s(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
 /* solver.py:202-230 sinkhorn_1d.  out_a/out_b receive the absorbed
- * shifts, hist[itr_max] the per-iteration errors, cost the W1 estimate. */
+ * shifts, hist[itr_max] the per-iteration errors, cost the W1 estimate.
+ * timing (nullable): setup s, loop s (the reference's wall_time -
+ * setup_time window, solver.py:172/:199), cost s. */
+int orc_sinkhorn_1d_timed(i64 n, const double *x, i64 m, const double *y, const double *u,
+                          const double *v, double eps, i64 itr_max, double tol, int stabilize,
+                          double thr, i64 check_every, double *phi, double *psi, double *out_a,
+                          double *out_b, double *hist, i64 *info, i64 *absorb_its, double *cost,
+                          double *timing);
 int orc_sinkhorn_1d(i64 n, const double *x, i64 m, const double *y, const double *u,
                     const double *v, double eps, i64 itr_max, double tol, int stabilize,
                     double thr, i64 check_every, double *phi, double *psi, double *out_a,
                     double *out_b, double *hist, i64 *info, i64 *absorb_its, double *cost) {
+    return orc_sinkhorn_1d_timed(n, x, m, y, u, v, eps, itr_max, tol, stabilize, thr,
+                                 check_every, phi, psi, out_a, out_b, hist, info, absorb_its,
+                                 cost, NULL);
+}
+
+int orc_sinkhorn_1d_timed(i64 n, const double *x, i64 m, const double *y, const double *u,
+                          const double *v, double eps, i64 itr_max, double tol, int stabilize,
+                          double thr, i64 check_every, double *phi, double *psi, double *out_a,
+                          double *out_b, double *hist, i64 *info, i64 *absorb_its, double *cost,
+                          double *timing) {
+    double t0 = now_s();
     if (n < 1 || m < 1 || !(eps > 0) || !isfinite(eps) || itr_max < 1) return ST_BADARG;
     ad1_t ad;
     memset(&ad, 0, sizeof(ad));
@@ -431,9 +457,13 @@ int orc_sinkhorn_1d(i64 n, const double *x, i64 m, const double *y, const double
     ad.t = malloc(sizeof(double) * m); ad.qm = malloc(sizeof(double) * m);
     ad.s = malloc(sizeof(double) * n); ad.qn = malloc(sizeof(double) * n);
     cfg_t c = {eps, itr_max, tol, stabilize, thr, check_every};
+    double t1 = now_s();
     int st = run_driver(&ad, ad1_iterate, ad1_absorb, u, n, v, m, &c, phi, psi, hist, info,
                         absorb_its);
+    double t2 = now_s();
     *cost = st == ST_OK ? cost_1d(&ad.op, x, y, phi, psi) : NAN;
+    double t3 = now_s();
+    if (timing) { timing[0] = t1 - t0; timing[1] = t2 - t1; timing[2] = t3 - t2; }
     op1_free(&ad.op);
     free(ad.t); free(ad.qm); free(ad.s); free(ad.qn);
     return st;

@@ -34,6 +34,8 @@ def load():
         lib.orc_sinkhorn_1d.restype = _i
         lib.orc_sinkhorn_1d.argtypes = [_i64, _vp, _i64, _vp, _vp, _vp, _d, _i64, _d, _i, _d,
                                         _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        lib.orc_sinkhorn_1d_timed.restype = _i
+        lib.orc_sinkhorn_1d_timed.argtypes = lib.orc_sinkhorn_1d.argtypes + [_vp]
         lib.orc_apply_1d.restype = _i
         lib.orc_apply_1d.argtypes = [_i64, _vp, _i64, _vp, _d, _vp, _vp, _vp, _i, _vp, _vp]
         lib.orc_cost_1d.restype = _i
@@ -71,12 +73,15 @@ def sinkhorn_1d(x, y, u, v, eps, itr_max, tol=0.0, stabilize=False, thr=200.0, c
     info = np.zeros(5, dtype=np.int64)
     abs_its = np.zeros(itr_max, dtype=np.int64)
     cost = np.zeros(1)
-    st = load().orc_sinkhorn_1d(n, _p(x), m, _p(y), _p(u), _p(v), eps, itr_max, tol,
-                                int(stabilize), thr, check_every, _p(phi), _p(psi), _p(a), _p(b),
-                                _p(hist), _p(info), _p(abs_its), _p(cost))
+    timing = np.zeros(3)
+    st = load().orc_sinkhorn_1d_timed(n, _p(x), m, _p(y), _p(u), _p(v), eps, itr_max, tol,
+                                      int(stabilize), thr, check_every, _p(phi), _p(psi), _p(a),
+                                      _p(b), _p(hist), _p(info), _p(abs_its), _p(cost),
+                                      _p(timing))
     return dict(status=st, phi=phi, psi=psi, a=a, b=b, hist=hist[:info[0]],
                 iterations=int(info[0]), converged=bool(info[1]), n_absorb=int(info[3]),
-                absorb_its=abs_its[:info[3]].copy(), cost=float(cost[0]))
+                absorb_its=abs_its[:info[3]].copy(), cost=float(cost[0]),
+                setup_s=float(timing[0]), loop_s=float(timing[1]), cost_s=float(timing[2]))
 
 
 def apply_1d(x, y, eps, vin, mode, a=None, b=None):

@@ -32,6 +32,9 @@ SIGNATURES = {
     "finom_cost1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "finom_apply1d": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _vp, _vp]),
     "finom_iterate1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_profile1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_int, _c_dbl,
+                                 _vp, _vp, _vp]),
+    "finom_solve1d_launches": (_c_i64, [_vp, _c_i64, _c_int]),
     "finom_sinkhorn1d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _vp, _vp, _c_dbl, _c_i64,
                                        _c_dbl, _c_int, _c_dbl, _vp, _vp, _vp, _vp, _vp, _vp,
                                        _vp, _vp, _vp]),
