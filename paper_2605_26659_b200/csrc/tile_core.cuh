@@ -25,7 +25,7 @@ constexpr int WPC = 4;                  // warps (tiles) per CTA
 constexpr int NTHR = 32 * WPC;
 constexpr int FAN = 32;                 // resolve-tree fan-out
 constexpr int NLEV = 5;                 // tiles + 4 levels (32^4 tiles per problem)
-static_assert(EPT <= 32, "walk mask is 32 bits");
+static_assert(EPT <= 32 && 32 % EPT == 0, "walk mask is 32 bits, lane chunks word-aligned");
 
 enum { ST_OK = 0, ST_ZD = 1, ST_NF = 2 };
 
@@ -159,14 +159,17 @@ __device__ __forceinline__ bool tree_arrive(const Resolve &R, const TreeGeo &tg,
                                             double (&top)[4]) {
   const int lane = threadIdx.x & 31;
   int idx = lt;
+#pragma unroll 1
   for (int L = 0; L + 1 < NLEV; ++L) {
     const int parent = idx / FAN;
     const int nchild = min(FAN, tg.n[L] - parent * FAN);
     Node *pn = R.lev[L + 1] + tg.base[L + 1] + parent;
     int last = 0;
     if (lane == 0) {
-      __threadfence();
-      last = atomicAdd(&pn->cnt, 1) == nchild - 1;
+      int old;
+      asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;"
+                   : "=r"(old) : "l"(&pn->cnt) : "memory");
+      last = old == nchild - 1;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) return false;
@@ -266,6 +269,30 @@ __device__ __forceinline__ void load_tab(double2 *tab) {
     tab[k] = make_double2(EXP_TAB_C[k][0], EXP_TAB_C[k][1]);
 }
 
+__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+// asynchronous dst[-1 .. cnt] <- src[lo-1 .. lo+cnt]; completes at cp_async_wait()
+__device__ __forceinline__ void load_halo_async(double *dst, const double *src, int lo, int cnt,
+                                                int N, bool zero) {
+  const int lane = threadIdx.x & 31;
+  if (zero) {
+    for (int k = lane - 1; k <= cnt; k += 32) dst[k] = 0.0;
+    return;
+  }
+  for (int k = lane; k < cnt; k += 32) cp_async8(dst + k, src + lo + k);
+  if (lane == 0) {
+    if (lo > 0) cp_async8(dst - 1, src + lo - 1); else dst[-1] = 0.0;
+  }
+  if (lane == 1) {
+    if (lo + cnt < N) cp_async8(dst + cnt, src + lo + cnt); else dst[cnt] = 0.0;
+  }
+}
+
 // dst[-1 .. cnt] <- src[lo-1 .. lo+cnt] (halo entries only where they exist)
 __device__ __forceinline__ void load_halo(double *dst, const double *src, int lo, int cnt, int N,
                                           bool zero) {
@@ -327,6 +354,43 @@ __device__ __forceinline__ Walk walk0(const Sm &s, int nr, int nc) {
   return w;
 }
 
+// Same chunk from the precomputed merged-order mask of the tile (8 words,
+// bit k = 1 iff merged element k is a column): no coordinate comparisons.
+__device__ __forceinline__ Walk walk_mask(const Sm &s, const unsigned *mw, int nr, int nc) {
+  const int lane = threadIdx.x & 31;
+  const int M = nr + nc;
+  Walk w;
+  const int pos0 = min(lane * EPT, M);
+  w.cnt = min(EPT, M - pos0);
+  unsigned bits = (__ldg(mw + (lane * EPT) / 32) >> ((lane * EPT) % 32)) & ((1u << EPT) - 1u);
+  bits &= w.cnt >= 32 ? 0xffffffffu : ((1u << w.cnt) - 1u);
+  const int pc = __popc(bits);
+  int incl = pc;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  w.jb = incl - pc;
+  w.ib = pos0 - w.jb;
+  int i = w.ib, j = w.jb;
+  for (int k = 0; k < w.cnt; ++k) {
+    const int slot = k * 32 + lane;
+    if ((bits >> k) & 1u) {
+      s.cown[j] = i;
+      s.cslot[j] = slot;
+      ++j;
+    } else {
+      s.rslot[i] = slot;
+      ++i;
+    }
+  }
+  w.ie = i;
+  w.je = j;
+  w.mask = bits;
+  return w;
+}
+
 struct Geo {  // roles of one half within a tile
   int r0, r1, nR, c0, c1, nC;
   double cfirst, clast, rfirst, rlast;
@@ -341,24 +405,16 @@ __device__ __forceinline__ void tile_ratios(const Sm &s, const Geo &g, int nr, b
   const int lane = threadIdx.x & 31;
 #pragma unroll 2
   for (int i = lane; i <= nr; i += 32) {
-    int gi = g.r0 + i;
-    double f = 0.0, b = 0.0;
-    if (gi > 0 && gi < g.nR) {
-      double gap = s.Rc[i] - s.Rc[i - 1];
-      bool pf = (i < nr) && (g.cfirst <= s.Rc[i - 1]);
-      bool pb = (i > 0) && (g.clast > s.Rc[i]);
-      if (absorbed) {
-        double da = s.Ra[i] - s.Ra[i - 1];
-        if (pf) f = ratio_exp(gap, da, true, eps, inv, tab);
-        if (pb) b = ratio_exp(gap, da, false, eps, inv, tab);
-      } else if (pf || pb) {
-        double e = ratio_exp(gap, 0.0, true, eps, inv, tab);
-        f = pf ? e : 0.0;
-        b = pb ? e : 0.0;
-      }
-    }
-    if (i < nr) s.vf[s.rslot[i]] = f;
-    if (i > 0) s.vb[s.rslot[i - 1]] = b;
+    const int gi = g.r0 + i;
+    const bool have = gi > 0 && gi < g.nR;
+    const double gap = have ? s.Rc[i] - s.Rc[i - 1] : 0.0;
+    const double da = (have && absorbed) ? s.Ra[i] - s.Ra[i - 1] : 0.0;
+    const bool pf = have && (i < nr) && (g.cfirst <= s.Rc[i - 1]);
+    const bool pb = have && (i > 0) && (g.clast > s.Rc[i]);
+    const double ef = ratio_exp(gap, da, true, eps, inv, tab);
+    const double eb = absorbed ? ratio_exp(gap, da, false, eps, inv, tab) : ef;
+    if (i < nr) s.vf[s.rslot[i]] = pf ? ef : 0.0;
+    if (i > 0) s.vb[s.rslot[i - 1]] = pb ? eb : 0.0;
   }
 }
 
@@ -370,17 +426,18 @@ __device__ __forceinline__ void tile_contrib(const Sm &s, const Geo &g, int nc, 
   const int lane = threadIdx.x & 31;
 #pragma unroll 2
   for (int j = lane; j < nc; j += 32) {
-    double c = s.Cc[j], ca = s.Ca[j];
+    const double c = s.Cc[j], ca = s.Ca[j];
     double v = s.Cv[j];
     if (ymul) v = c * v;
-    int o = s.cown[j];
-    int og = g.r0 + o;
-    double lo = 0.0, hi = 0.0;
-    if (og < g.nR) lo = edge_exp(s.Rc[o] - c, s.Ra[o], ca, eps, inv, tab) * v;
-    if (og > 0) hi = edge_exp(c - s.Rc[o - 1], s.Ra[o - 1], ca, eps, inv, tab) * v;
+    const int o = s.cown[j];
+    const int og = g.r0 + o;
+    // both exponentials unconditionally (independent chains interleave);
+    // the halo entries beyond the mesh ends are finite placeholders
+    const double elo = edge_exp(s.Rc[o] - c, s.Ra[o], ca, eps, inv, tab);
+    const double ehi = edge_exp(c - s.Rc[o - 1], s.Ra[o - 1], ca, eps, inv, tab);
     const int sl = s.cslot[j];
-    s.vf[sl] = lo;
-    s.vb[sl] = hi;
+    s.vf[sl] = og < g.nR ? elo * v : 0.0;
+    s.vb[sl] = og > 0 ? ehi * v : 0.0;
   }
 }
 
@@ -464,14 +521,15 @@ __device__ __forceinline__ void next_contrib2(const double *Nc, const double *Na
                                               int c1, int nNR, double c, double ca, double v,
                                               double eps, double inv, const double2 *tab,
                                               double &fC, double &fE, double &bC, double &bE) {
-  if (nn > 0 && c <= Nc[nn - 1])
-    fC += edge_exp(Nc[nn - 1] - c, Na[nn - 1], ca, eps, inv, tab) * v;
-  else if (c1 < nNR)
-    fE += edge_exp(Nc[nn] - c, Na[nn], ca, eps, inv, tab) * v;
-  if (nn > 0 && c > Nc[0])
-    bC += edge_exp(c - Nc[0], Na[0], ca, eps, inv, tab) * v;
-  else if (c0 > 0)
-    bE += edge_exp(c - Nc[-1], Na[-1], ca, eps, inv, tab) * v;
+  const bool fin = nn > 0 && c <= Nc[nn - 1];  // before the last next row
+  const bool bin = nn > 0 && c > Nc[0];        // after the first next row
+  const int fk = fin ? nn - 1 : nn, bk = bin ? 0 : -1;
+  const double ef = edge_exp(Nc[fk] - c, Na[fk], ca, eps, inv, tab) * v;
+  const double eb = edge_exp(c - Nc[bk], Na[bk], ca, eps, inv, tab) * v;
+  if (fin) fC += ef;
+  else if (c1 < nNR) fE += ef;
+  if (bin) bC += eb;
+  else if (c0 > 0) bE += eb;
 }
 
 // Composite coefficients of the next-half maps (each the product the
@@ -489,15 +547,13 @@ __device__ __forceinline__ void next_maps(const double *Nc, const double *Na, in
     mb = Tf{1.0, 0.0, 0.0, 1.0, bE};
     return;
   }
+  // lane 0: fB (c0 -> c1-1), 1: fA (c0-1 -> c1-1), 2: bB (c1-1 -> c0), 3: bA (c1 -> c0)
+  const int hi = (lane == 3) ? nn : nn - 1;
+  const int lo = (lane == 1) ? -1 : 0;
+  const bool use = lane < 4 && (lane == 0 || lane == 2 || (lane == 1 && c0 > 0 && kfirst <= Nc[-1]) ||
+                                (lane == 3 && c1 < nNR && klast > Nc[nn]));
   double e = 0.0;
-  if (lane == 0)
-    e = ratio_exp(Nc[nn - 1] - Nc[0], Na[nn - 1] - Na[0], true, eps, inv, tab);
-  else if (lane == 1 && c0 > 0 && kfirst <= Nc[-1])
-    e = ratio_exp(Nc[nn - 1] - Nc[-1], Na[nn - 1] - Na[-1], true, eps, inv, tab);
-  else if (lane == 2)
-    e = ratio_exp(Nc[nn - 1] - Nc[0], Na[nn - 1] - Na[0], false, eps, inv, tab);
-  else if (lane == 3 && c1 < nNR && klast > Nc[nn])
-    e = ratio_exp(Nc[nn] - Nc[0], Na[nn] - Na[0], false, eps, inv, tab);
+  if (use) e = ratio_exp(Nc[hi] - Nc[lo], Na[hi] - Na[lo], lane < 2, eps, inv, tab);
   const double fB = __shfl_sync(0xffffffffu, e, 0), fA = __shfl_sync(0xffffffffu, e, 1);
   const double bB = __shfl_sync(0xffffffffu, e, 2), bA = __shfl_sync(0xffffffffu, e, 3);
   mf = Tf{fA, fB, fC, 0.0, fE};
