@@ -7,7 +7,7 @@ public names mirror ``finom.solver``, ``finom.kernel1d`` and
 include/finom_b200.h.
 """
 
-from . import errors, kernel1d, mesh, solver  # noqa: F401
+from . import errors, kernel1d, kernel2d, mesh, solver  # noqa: F401
 from .errors import *  # noqa: F401,F403
 from .mesh import Grid2D, Measure, Measure2D, Mesh1D, Problem  # noqa: F401
 from .solver import (  # noqa: F401
@@ -23,5 +23,6 @@ from .solver import (  # noqa: F401
     sinkhorn_1d_batched,
     transport_cost_fast,
 )
+from .kernel2d import KernelOperator2D, build_operator_2d, sinkhorn_2d, transport_cost_fast_2d  # noqa: F401,E501
 
 __version__ = "0.1.0"

@@ -178,4 +178,24 @@ FB_HD double ratio_exp(double g, double da, bool lower, double eps, double inv,
   return fexp(q_div(num, eps, inv), tab);
 }
 
+// Dynamic-shift forms of the 2D sweeps (_kernels.py:140-159):
+//   edge  exp(((a_o + b_t) - d) * inv_eps)
+//   ratio exp(((a_i - a_{i-1}) - g) * inv_eps)   lower, da = a_i - a_{i-1}
+//         exp(((a_{i-1} - a_i) - g) * inv_eps)   upper (row i-1 from row i)
+FB_HD double edge_exp_dyn(double d, double ar, double ac, double inv, const double2* tab) {
+  return fexp(FB_MUL(FB_SUB(FB_ADD(ar, ac), d), inv), tab);
+}
+FB_HD double ratio_exp_dyn(double g, double da, bool lower, double inv, const double2* tab) {
+  return fexp(FB_MUL(FB_SUB(lower ? da : -da, g), inv), tab);
+}
+// Either form (dyn selects the 2D-absorbed expression).
+FB_HD double edge_x(bool dyn, double d, double ar, double ac, double eps, double inv,
+                    const double2* tab) {
+  return dyn ? edge_exp_dyn(d, ar, ac, inv, tab) : edge_exp(d, ar, ac, eps, inv, tab);
+}
+FB_HD double ratio_x(bool dyn, double g, double da, bool lower, double eps, double inv,
+                     const double2* tab) {
+  return dyn ? ratio_exp_dyn(g, da, lower, inv, tab) : ratio_exp(g, da, lower, eps, inv, tab);
+}
+
 }  // namespace fb

@@ -401,7 +401,8 @@ struct Geo {  // roles of one half within a tile
 //   vf[row i]   = r_lo into row i     (0 if no column <= row i-1)
 //   vb[row i-1] = r_hi out of row i-1 (0 if no column >  row i)
 __device__ __forceinline__ void tile_ratios(const Sm &s, const Geo &g, int nr, bool absorbed,
-                                            double eps, double inv, const double2 *tab) {
+                                            double eps, double inv, const double2 *tab,
+                                            bool dyn = false) {
   const int lane = threadIdx.x & 31;
 #pragma unroll 2
   for (int i = lane; i <= nr; i += 32) {
@@ -411,8 +412,8 @@ __device__ __forceinline__ void tile_ratios(const Sm &s, const Geo &g, int nr, b
     const double da = (have && absorbed) ? s.Ra[i] - s.Ra[i - 1] : 0.0;
     const bool pf = have && (i < nr) && (g.cfirst <= s.Rc[i - 1]);
     const bool pb = have && (i > 0) && (g.clast > s.Rc[i]);
-    const double ef = ratio_exp(gap, da, true, eps, inv, tab);
-    const double eb = absorbed ? ratio_exp(gap, da, false, eps, inv, tab) : ef;
+    const double ef = ratio_x(dyn, gap, da, true, eps, inv, tab);
+    const double eb = absorbed ? ratio_x(dyn, gap, da, false, eps, inv, tab) : ef;
     if (i < nr) s.vf[s.rslot[i]] = pf ? ef : 0.0;
     if (i > 0) s.vb[s.rslot[i - 1]] = pb ? eb : 0.0;
   }
@@ -422,7 +423,8 @@ __device__ __forceinline__ void tile_ratios(const Sm &s, const Geo &g, int nr, b
 // o = cown[j] (kernel1d.py:148; edge times value as in _kernels.py:283/:288).
 // v_j = Cv[j] (times the column coordinate if ymul).
 __device__ __forceinline__ void tile_contrib(const Sm &s, const Geo &g, int nc, bool ymul,
-                                             double eps, double inv, const double2 *tab) {
+                                             double eps, double inv, const double2 *tab,
+                                             bool dyn = false) {
   const int lane = threadIdx.x & 31;
 #pragma unroll 2
   for (int j = lane; j < nc; j += 32) {
@@ -433,8 +435,8 @@ __device__ __forceinline__ void tile_contrib(const Sm &s, const Geo &g, int nc, 
     const int og = g.r0 + o;
     // both exponentials unconditionally (independent chains interleave);
     // the halo entries beyond the mesh ends are finite placeholders
-    const double elo = edge_exp(s.Rc[o] - c, s.Ra[o], ca, eps, inv, tab);
-    const double ehi = edge_exp(c - s.Rc[o - 1], s.Ra[o - 1], ca, eps, inv, tab);
+    const double elo = edge_x(dyn, s.Rc[o] - c, s.Ra[o], ca, eps, inv, tab);
+    const double ehi = edge_x(dyn, c - s.Rc[o - 1], s.Ra[o - 1], ca, eps, inv, tab);
     const int sl = s.cslot[j];
     s.vf[sl] = og < g.nR ? elo * v : 0.0;
     s.vb[sl] = og > 0 ? ehi * v : 0.0;
@@ -520,12 +522,13 @@ __device__ __forceinline__ void tile_states(const Sm &s, const Walk &w, double &
 __device__ __forceinline__ void next_contrib2(const double *Nc, const double *Na, int nn, int c0,
                                               int c1, int nNR, double c, double ca, double v,
                                               double eps, double inv, const double2 *tab,
-                                              double &fC, double &fE, double &bC, double &bE) {
+                                              double &fC, double &fE, double &bC, double &bE,
+                                              bool dyn = false) {
   const bool fin = nn > 0 && c <= Nc[nn - 1];  // before the last next row
   const bool bin = nn > 0 && c > Nc[0];        // after the first next row
   const int fk = fin ? nn - 1 : nn, bk = bin ? 0 : -1;
-  const double ef = edge_exp(Nc[fk] - c, Na[fk], ca, eps, inv, tab) * v;
-  const double eb = edge_exp(c - Nc[bk], Na[bk], ca, eps, inv, tab) * v;
+  const double ef = edge_x(dyn, Nc[fk] - c, Na[fk], ca, eps, inv, tab) * v;
+  const double eb = edge_x(dyn, c - Nc[bk], Na[bk], ca, eps, inv, tab) * v;
   if (fin) fC += ef;
   else if (c1 < nNR) fE += ef;
   if (bin) bC += eb;
@@ -540,7 +543,7 @@ __device__ __forceinline__ void next_contrib2(const double *Nc, const double *Na
 __device__ __forceinline__ void next_maps(const double *Nc, const double *Na, int nn, int c0,
                                           int c1, int nNR, double kfirst, double klast, double fC,
                                           double fE, double bC, double bE, double eps, double inv,
-                                          const double2 *tab, Tf &mf, Tf &mb) {
+                                          const double2 *tab, Tf &mf, Tf &mb, bool dyn = false) {
   const int lane = threadIdx.x & 31;
   if (nn == 0) {
     mf = Tf{1.0, 0.0, 0.0, 1.0, fE};
@@ -553,7 +556,7 @@ __device__ __forceinline__ void next_maps(const double *Nc, const double *Na, in
   const bool use = lane < 4 && (lane == 0 || lane == 2 || (lane == 1 && c0 > 0 && kfirst <= Nc[-1]) ||
                                 (lane == 3 && c1 < nNR && klast > Nc[nn]));
   double e = 0.0;
-  if (use) e = ratio_exp(Nc[hi] - Nc[lo], Na[hi] - Na[lo], lane < 2, eps, inv, tab);
+  if (use) e = ratio_x(dyn, Nc[hi] - Nc[lo], Na[hi] - Na[lo], lane < 2, eps, inv, tab);
   const double fB = __shfl_sync(0xffffffffu, e, 0), fA = __shfl_sync(0xffffffffu, e, 1);
   const double bB = __shfl_sync(0xffffffffu, e, 2), bA = __shfl_sync(0xffffffffu, e, 3);
   mf = Tf{fA, fB, fC, 0.0, fE};

@@ -97,3 +97,47 @@ def config5_problem(p, n=16_384, seed=505):
 def config5(batch=8192, n=16_384, seed=505, problems=None):
     idx = range(batch) if problems is None else problems
     return [config5_problem(p, n, seed) for p in idx]
+
+
+def tanh_nodes(n):
+    """x_k = 0.5 + 0.5 tanh(3(2k/n - 1)) / tanh(3), k = 0..n-1 (clustered at the edges)."""
+    k = np.arange(n, dtype=np.float64)
+    return 0.5 + 0.5 * np.tanh(3.0 * (2.0 * k / n - 1.0)) / np.tanh(3.0)
+
+
+def blobs(x, y, rng, nblob):
+    """Seeded anisotropic, rotated Gaussian blobs on the grid x (rows) by y (cols)."""
+    X, Y = np.meshgrid(x, y, indexing="ij")
+    dens = np.zeros_like(X)
+    wts = rng.dirichlet(np.ones(nblob))
+    for b in range(nblob):
+        cx, cy = rng.uniform(0.2, 0.8, 2)
+        sx, sy = rng.uniform(0.05, 0.15, 2)
+        th = rng.uniform(0.0, np.pi)
+        c, s = np.cos(th), np.sin(th)
+        dx, dy = X - cx, Y - cy
+        u = (c * dx + s * dy) / sx
+        v = (-s * dx + c * dy) / sy
+        dens += wts[b] * np.exp(-0.5 * (u * u + v * v))
+    w = dens * np.outer(cell_widths(x), cell_widths(y))
+    return w / w.sum()
+
+
+def config3(n=1024, seed=303):
+    """2D, tanh-stretched tensor grid (source == target), 2 / 3 blobs, eps = 5e-3."""
+    rng = np.random.default_rng(seed)
+    x = tanh_nodes(n)
+    y = tanh_nodes(n)
+    U = blobs(x, y, rng, 2)
+    V = blobs(x, y, rng, 3)
+    return x, y, x.copy(), y.copy(), U, V, 5e-3
+
+
+def config4(n=8192, seed=404):
+    """2D, random-gap grid U[0.1,1.9] per axis (source == target), 8 blobs each, eps = 1e-3."""
+    rng = np.random.default_rng(seed)
+    x = gap_mesh(rng, n, 0.1, 1.9)
+    y = gap_mesh(rng, n, 0.1, 1.9)
+    U = blobs(x, y, rng, 8)
+    V = blobs(x, y, rng, 8)
+    return x, y, x.copy(), y.copy(), U, V, 1e-3

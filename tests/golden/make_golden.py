@@ -223,3 +223,101 @@ if __name__ == "__main__":
         config_runs()
     if "config2_full" in which:
         config2_full()
+
+
+def ref_solve_2d(x1, y1, x2, y2, U, V, cfg):
+    """kernel2d.sinkhorn_2d (kernel2d.py:363-391) with absorb iterations recorded."""
+    src = rm.Grid2D(rm.Mesh1D(x1), rm.Mesh1D(y1))
+    tgt = rm.Grid2D(rm.Mesh1D(x2), rm.Mesh1D(y2))
+    ad = r2._GridAdapter(src, tgt, cfg.epsilon)
+    calls, absorbs = [0], []
+    it0, ab0 = ad.iterate, ad.absorb
+    def it(*a):
+        calls[0] += 1
+        return it0(*a)
+    def ab(da, db):
+        absorbs.append(calls[0])
+        ab0(da, db)
+    ad.iterate, ad.absorb = it, ab
+    uw = np.ascontiguousarray(U.ravel(order="F"))
+    vw = np.ascontiguousarray(V.ravel(order="F"))
+    phi, psi, its, conv, hist, loop = rs.run_driver(ad, uw, vw, cfg)
+    sol = rs.Solution(phi=phi, psi=psi, a=ad.a, b=ad.b, kernel=ad.kernel, iterations_run=its,
+                      converged=conv, marginal_error_history=hist, wall_time=loop,
+                      setup_time=0.0, cost=np.nan, config=cfg)
+    sol.cost = r2.transport_cost_fast_2d(sol)
+    return dict(phi=phi, psi=psi, a=np.asarray(ad.a), b=np.asarray(ad.b),
+                hist_it=np.array([h[0] for h in hist], dtype=np.int64),
+                hist_err=np.array([h[1] for h in hist]), iterations=its, converged=conv,
+                absorb_its=np.array(absorbs, dtype=np.int64), cost=sol.cost, loop_s=loop)
+
+
+def grid_cases():
+    """2D runs (no kernel2d test exists in the reference: SURVEY.md 8(c))."""
+    out = {}
+    rng = np.random.default_rng(77)
+    cases = []
+    def rnd(n):
+        return rm.random_sorted_nodes(n, int(rng.integers(2**31))).nodes
+    for (n1, m1, n2, m2, eps, stab, thr, itr) in [
+        (6, 5, 4, 7, 0.1, False, 200.0, 60), (6, 5, 4, 7, 0.05, True, 2.0, 80),
+        (12, 9, 10, 11, 0.05, False, 200.0, 100), (12, 9, 10, 11, 0.02, True, 3.0, 150),
+        (40, 33, 37, 41, 0.01, True, 20.0, 120)]:
+        x1, y1, x2, y2 = rnd(n1), rnd(m1), rnd(n2), rnd(m2)
+        U = rng.random((n1, m1)) + 0.05
+        V = rng.random((n2, m2)) + 0.05
+        U /= U.sum()
+        V /= V.sum()
+        cases.append((x1, y1, x2, y2, U, V, rs.SolverConfig(epsilon=eps, itr_max=itr, tol=0.0,
+                                                            stabilize=stab, absorb_threshold=thr)))
+    x1, y1, x2, y2, U, V, eps = W.config3(n=64)
+    cases.append((x1, y1, x2, y2, U, V, rs.SolverConfig(epsilon=eps, itr_max=300, tol=0.0,
+                                                        stabilize=True)))
+    x1, y1, x2, y2, U, V, eps = W.config4(n=96)
+    cases.append((x1, y1, x2, y2, U, V, rs.SolverConfig(epsilon=eps, itr_max=100, tol=0.0,
+                                                        stabilize=True)))
+    for k, (x1, y1, x2, y2, U, V, cfg) in enumerate(cases):
+        r = ref_solve_2d(x1, y1, x2, y2, U, V, cfg)
+        for key, val in dict(x1=x1, y1=y1, x2=x2, y2=y2, U=U, V=V).items():
+            out["g%d_%s" % (k, key)] = val
+        out["g%d_cfg" % k] = np.array([cfg.epsilon, cfg.itr_max, cfg.tol, float(cfg.stabilize),
+                                       cfg.absorb_threshold, cfg.check_every])
+        for key, val in r.items():
+            out["g%d_%s" % (k, key)] = np.asarray(val)
+        # operator applies on the final (absorbed) kernel
+        op = r2.build_operator_2d(rm.Grid2D(rm.Mesh1D(x1), rm.Mesh1D(y1)),
+                                  rm.Grid2D(rm.Mesh1D(x2), rm.Mesh1D(y2)), cfg.epsilon)
+        vin = rng.random(len(x2) * len(y2))
+        win = rng.random(len(x1) * len(y1))
+        out["g%d_vin" % k] = vin
+        out["g%d_win" % k] = win
+        out["g%d_Kv" % k] = op.apply(vin)
+        out["g%d_KTw" % k] = op.apply_transpose(win)
+        A = r["a"].reshape((len(x1), len(y1)), order="F")
+        B = r["b"].reshape((len(x2), len(y2)), order="F")
+        if np.any(A != 0) or np.any(B != 0):
+            opa = op.absorb(A, B)
+            out["g%d_Kv_abs" % k] = opa.apply(vin)
+            out["g%d_KTw_abs" % k] = opa.apply_transpose(win)
+    out["ncases"] = np.array(len(cases))
+    save("grid_cases.npz", **out)
+
+
+def config3_full():
+    x1, y1, x2, y2, U, V, eps = W.config3()
+    t = time.time()
+    r = ref_solve_2d(x1, y1, x2, y2, U, V, rs.SolverConfig(epsilon=eps, itr_max=300, tol=0.0,
+                                                           stabilize=True))
+    dt = time.time() - t
+    stride = 997
+    save("config3_full_pins.npz", cost=np.array(r["cost"]), hist_err=r["hist_err"],
+         absorb_its=r["absorb_its"], iterations=np.array(r["iterations"]), stride=np.array(stride),
+         phi_s=r["phi"][::stride], psi_s=r["psi"][::stride], a_s=r["a"][::stride],
+         b_s=r["b"][::stride], loop_s=np.array(r["loop_s"]), ref_wall_s=np.array(dt))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    if "grid" in sys.argv[1:]:
+        grid_cases()
+    if "config3_full" in sys.argv[1:]:
+        config3_full()

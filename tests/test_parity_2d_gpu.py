@@ -1,0 +1,79 @@
+"""2D grid path (kernel2d) vs the reference (golden fixtures) and the C oracle.
+
+The reference ships no kernel2d tests; tests/golden/
+make_golden.py records the reference's own sinkhorn_2d / operator outputs.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2605_26659_b200 as fb
+from paper_2605_26659_b200 import kernel2d as k2
+from paper_2605_26659_b200 import workloads as W
+
+from conftest import GOLDEN, load_golden, rel_inf
+from test_parity_gpu import TOL, _check_solution
+
+pytestmark = pytest.mark.gpu
+
+
+def _grid(x, y):
+    return fb.Grid2D(fb.Mesh1D(x), fb.Mesh1D(y))
+
+
+def test_grid_cases_vs_reference():
+    g = load_golden("grid_cases.npz")
+    for k in range(int(g["ncases"])):
+        c = lambda key: g["g%d_%s" % (k, key)]
+        eps, itr, tol, stab, thr, ce = c("cfg")
+        cfg = fb.SolverConfig(epsilon=eps, itr_max=int(itr), tol=tol, stabilize=bool(stab),
+                              absorb_threshold=thr, check_every=int(ce))
+        src, tgt = _grid(c("x1"), c("y1")), _grid(c("x2"), c("y2"))
+        sol = fb.sinkhorn_2d(src, tgt, fb.Measure2D(c("U")), fb.Measure2D(c("V")), cfg)
+        r = {key: c(key) for key in ("phi", "psi", "a", "b", "hist_it", "hist_err",
+                                     "iterations", "converged", "absorb_its", "cost")}
+        _check_solution(sol, r)
+        op = k2.build_operator_2d(src, tgt, eps)
+        assert rel_inf(op.apply(c("vin")), c("Kv")) < 1e-12, k
+        assert rel_inf(op.apply_transpose(c("win")), c("KTw")) < 1e-12, k
+        if "g%d_Kv_abs" % k in g:
+            A = c("a").reshape((len(c("x1")), len(c("y1"))), order="F")
+            B = c("b").reshape((len(c("x2")), len(c("y2"))), order="F")
+            opa = op.absorb(A, B)
+            assert rel_inf(opa.apply(c("vin")), c("Kv_abs")) < 1e-12, k
+            assert rel_inf(opa.apply_transpose(c("win")), c("KTw_abs")) < 1e-12, k
+
+
+def test_cost_2d_state_vs_oracle():
+    from oracle import oracle as O
+    x1, y1, x2, y2, U, V, eps = W.config3(n=48)
+    r = O.sinkhorn_2d(x1, y1, x2, y2, U, V, eps, 80, 0.0, True, 30.0)
+    src, tgt = _grid(x1, y1), _grid(x2, y2)
+    sol = fb.sinkhorn_2d(src, tgt, fb.Measure2D(U), fb.Measure2D(V),
+                         fb.SolverConfig(epsilon=eps, itr_max=80, tol=0.0, stabilize=True,
+                                         absorb_threshold=30.0))
+    assert list(sol.absorb_iterations) == list(r["absorb_its"])
+    assert rel_inf(sol.phi, r["phi"]) < TOL and rel_inf(sol.psi, r["psi"]) < TOL
+    assert abs(sol.cost - r["cost"]) <= TOL * abs(r["cost"])
+    # the standalone cost entry on the same state
+    c = k2.transport_cost_fast_2d(sol)
+    assert abs(c - r["cost"]) <= TOL * abs(r["cost"])
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "config3_full_pins.npz")),
+                    reason="config-3 pins not generated")
+def test_config3_full_vs_reference_pins():
+    g = load_golden("config3_full_pins.npz")
+    x1, y1, x2, y2, U, V, eps = W.config3()
+    sol = fb.sinkhorn_2d(_grid(x1, y1), _grid(x2, y2), fb.Measure2D(U), fb.Measure2D(V),
+                         fb.SolverConfig(epsilon=eps, itr_max=300, tol=0.0, stabilize=True))
+    st = int(g["stride"])
+    from test_parity_gpu import hist_ok
+    q = dict(hist=hist_ok([h[1] for h in sol.marginal_error_history], g["hist_err"]),
+             phi=rel_inf(sol.phi[::st], g["phi_s"]), psi=rel_inf(sol.psi[::st], g["psi_s"]),
+             cost=abs(sol.cost - float(g["cost"])) / abs(float(g["cost"])))
+    print("config3 full parity", q)
+    assert list(sol.absorb_iterations) == [int(t) for t in g["absorb_its"]]
+    assert q["hist"] < 1 and q["phi"] < TOL and q["psi"] < TOL and q["cost"] < TOL, q

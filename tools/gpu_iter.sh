@@ -1,6 +1,6 @@
 # quick loop: smoke + parity tests + bench (no cpu baseline)
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
-timeout 600 python -m pytest tests/test_parity_gpu.py -q -m gpu -s -x 2>&1 | grep -E "passed|failed|Error|error|parity|^E " | head -20
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_parity_2d_gpu.py -q -m gpu -s -x 2>&1 | grep -E "passed|failed|Error|error|parity|^E " | head -20
 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -2 | python -c "
 import json,sys
 for l in sys.stdin:
