@@ -128,7 +128,46 @@ def workload(cfg, rank=0, world=1):
         return dict(xs=[p[0] for p in probs], ys=[p[1] for p in probs],
                     us=[p[2] for p in probs], vs=[p[3] for p in probs],
                     eps=[p[4] for p in probs], itr=200, name="config5", batch=B)
+    if cfg in (3, 4):
+        x1, y1, x2, y2, U, V, eps = W.config3() if cfg == 3 else W.config4()
+        return dict(grid=(x1, y1, x2, y2, U, V), eps=[eps], itr=300 if cfg == 3 else 100,
+                    name="config%d" % cfg)
     raise SystemExit("unknown config %r" % cfg)
+
+
+def run_2d(args, cfg, wl):
+    """2D configs (3: 1024^2, 4: 8192^2): finom_sinkhorn2d_host; value from its loop window."""
+    import paper_2605_26659_b200 as fb
+    x1, y1, x2, y2, U, V = wl["grid"]
+    src = fb.Grid2D(fb.Mesh1D(x1), fb.Mesh1D(y1))
+    tgt = fb.Grid2D(fb.Mesh1D(x2), fb.Mesh1D(y2))
+    scfg = fb.SolverConfig(epsilon=wl["eps"][0], itr_max=wl["itr"], tol=0.0, stabilize=True)
+    mu, mv = fb.Measure2D(U), fb.Measure2D(V)
+    pts = x1.size * y1.size
+    for _ in range(max(1, min(args.warmup, 2))):
+        fb.sinkhorn_2d(src, tgt, mu, mv, scfg)
+    loops, walls = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        sol = fb.sinkhorn_2d(src, tgt, mu, mv, scfg)
+        walls.append(time.perf_counter() - t0)
+        loops.append(sol.wall_time - sol.setup_time)
+    loop = statistics.median(loops)
+    line = {
+        "metric": METRIC, "value": pts * wl["itr"] / loop, "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * loop,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, BASELINE.json shapes; see DESIGN.md)",
+        "config": {"workload": "config%d: 2D %dx%d eps=%g %d it (stabilize=True)" % (
+            cfg, x1.size, y1.size, wl["eps"][0], wl["itr"]), "itr_max": wl["itr"],
+            "timing": "loop window of sinkhorn_2d (host-driven loop, one sync per iteration)"},
+        "e2e": {"value": pts * wl["itr"] / statistics.median(walls), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * (2 * pts + 2 * x1.size + 2 * y1.size),
+                "d2h_bytes_per_step": 8 * 4 * pts},
+        "iterations_run": sol.iterations_run, "absorbs": sol.absorb_iterations,
+        "cost": sol.cost,
+    }
+    print(json.dumps(line), flush=True)
 
 
 def config_json(cfg, wl, world):
@@ -205,7 +244,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 5])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -223,6 +262,10 @@ def main():
 
     cfg = args.config
     wl = workload(cfg, rank, world)
+    if cfg in (3, 4):
+        if rank == 0:
+            run_2d(args, cfg, wl)
+        return
     itr = wl["itr"]
     bs = fb.BatchSolver1D(wl["xs"], wl["ys"], wl["us"], wl["vs"], wl["eps"])
     pts = int(sum(x.size for x in wl["xs"]))

@@ -52,6 +52,13 @@ int finom_plan1d_create(int64_t P, const int64_t *xoff_host, const double *x_hos
                         const int64_t *yoff_host, const double *y_host,
                         const double *eps_host, void *stream, finom_plan1d **plan_out);
 int finom_plan1d_destroy(finom_plan1d *plan);
+
+/* Host-only: the merge-path tile partition of one mesh pair and the
+ * merged-order masks the kernels walk (no CUDA call; for tests).  Returns the
+ * tile count; fills up to max_tiles entries of tiles4 (x0, x1, y0, y1) and
+ * masks16 (8 words half A order | 8 words half B order, bit = column). */
+int64_t finom_tile_partition(int64_t n, const double *x, int64_t m, const double *y,
+                             int64_t max_tiles, int32_t *tiles4, uint32_t *masks16);
 /* Number of tiles, points etc. (for tests and bench accounting). */
 int finom_plan1d_info(const finom_plan1d *plan, int64_t *info8);
 

@@ -26,6 +26,7 @@ SIGNATURES = {
     "finom_build_info": (ctypes.c_char_p, []),
     "finom_plan1d_create": (_c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "finom_plan1d_destroy": (_c_int, [_vp]),
+    "finom_tile_partition": (_c_i64, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _vp]),
     "finom_plan1d_info": (_c_int, [_vp, _vp]),
     "finom_solve1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int,
                                _c_dbl, _vp, _vp, _vp, _vp]),
@@ -68,6 +69,18 @@ def load(require_device=True):
         if not torch.cuda.is_available():
             raise DeviceError("no CUDA device visible; the FINOM B200 path has no CPU fallback")
     return _lib
+
+
+def tile_partition(x, y):
+    """Host-only tile partition + merged-order masks (finom_tile_partition)."""
+    lib = load(require_device=False)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    T = lib.finom_tile_partition(x.size, ptr(x), y.size, ptr(y), 0, None, None)
+    tiles = np.zeros((T, 4), dtype=np.int32)
+    masks = np.zeros((T, 16), dtype=np.uint32)
+    lib.finom_tile_partition(x.size, ptr(x), y.size, ptr(y), T, ptr(tiles), ptr(masks))
+    return tiles, masks
 
 
 def last_error():

@@ -321,3 +321,21 @@ if __name__ == "__main__" and len(sys.argv) > 1:
         grid_cases()
     if "config3_full" in sys.argv[1:]:
         config3_full()
+
+
+def config4_full():
+    """Full-size config-4 pins (the reference takes ~20 min on one core)."""
+    x1, y1, x2, y2, U, V, eps = W.config4()
+    t = time.time()
+    r = ref_solve_2d(x1, y1, x2, y2, U, V, rs.SolverConfig(epsilon=eps, itr_max=100, tol=0.0,
+                                                           stabilize=True))
+    dt = time.time() - t
+    stride = 65521
+    save("config4_full_pins.npz", cost=np.array(r["cost"]), hist_err=r["hist_err"],
+         absorb_its=r["absorb_its"], iterations=np.array(r["iterations"]), stride=np.array(stride),
+         phi_s=r["phi"][::stride], psi_s=r["psi"][::stride], a_s=r["a"][::stride],
+         b_s=r["b"][::stride], loop_s=np.array(r["loop_s"]), ref_wall_s=np.array(dt))
+
+
+if __name__ == "__main__" and "config4_full" in sys.argv[1:]:
+    config4_full()

@@ -1,0 +1,111 @@
+"""The C-ABI library: builds for sm_100a, loads without a GPU, exports every
+symbol include/finom_b200.h declares; host-only entry points behave."""
+
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "finom_b200.h")
+
+
+def declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(finom_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_entry_points():
+    names = declared()
+    for must in ("finom_plan1d_create", "finom_solve1d", "finom_cost1d", "finom_apply1d",
+                 "finom_iterate1d", "finom_sinkhorn1d_host", "finom_sinkhorn2d_host",
+                 "finom_apply2d_host", "finom_cost2d_host"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2605_26659_b200 import _lib
+    lib = _lib.load(require_device=False)
+    for name in declared():
+        assert hasattr(lib, name), name
+    assert set(_lib.SIGNATURES) >= set(declared()) - {"finom_phase_read"}
+
+
+def test_library_is_sm100a():
+    from paper_2605_26659_b200 import _lib
+    info = _lib.load(require_device=False).finom_build_info().decode()
+    assert "sm_100a" in info
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True)
+    if out.returncode == 0:
+        assert "sm_100a" in out.stdout
+
+
+def test_no_cpu_fallback_without_device():
+    """The product path fails loudly when no CUDA device is present."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2605_26659_b200 as fb
+    x = fb.Mesh1D(np.linspace(0, 1, 5))
+    u = fb.Measure(np.full(5, 0.2))
+    with pytest.raises(fb.DeviceError):
+        fb.sinkhorn_1d(x, x, u, u, fb.SolverConfig(epsilon=0.1, itr_max=3))
+
+
+def _merge_ref(x, y, half):
+    """Merged order bits by a plain two-pointer merge (col first on ties)."""
+    bits, i, j = [], 0, 0
+    while i < x.size or j < y.size:
+        if half == 0:  # rows y, cols x: x_i <= y_j first
+            col = i < x.size and (j == y.size or x[i] <= y[j])
+            bits.append(col)
+            i, j = (i + 1, j) if col else (i, j + 1)
+        else:          # rows x, cols y: y_j <= x_i first
+            col = j < y.size and (i == x.size or y[j] <= x[i])
+            bits.append(col)
+            i, j = (i, j + 1) if col else (i + 1, j)
+    return bits
+
+
+@pytest.mark.parametrize("n,m,ties", [(1, 1, False), (5, 3, False), (700, 900, False),
+                                      (1000, 1000, True), (3000, 17, False)])
+def test_tile_partition_properties(n, m, ties):
+    from paper_2605_26659_b200 import _lib
+    rng = np.random.default_rng(n + m)
+    x = np.sort(rng.uniform(0, 1, n))
+    y = x.copy() if ties else np.sort(rng.uniform(0, 1, m))
+    tiles, masks = _lib.tile_partition(x, y)
+    assert tiles[0, 0] == 0 and tiles[0, 2] == 0
+    assert tiles[-1, 1] == x.size and tiles[-1, 3] == y.size
+    for t in range(len(tiles)):
+        x0, x1, y0, y1 = tiles[t]
+        if t:
+            assert x0 == tiles[t - 1, 1] and y0 == tiles[t - 1, 3]
+        assert 0 < (x1 - x0) + (y1 - y0) <= 256
+        # no tie pair split across tiles: tile elements strictly above the previous tile's
+        here = np.concatenate([x[x0:x1], y[y0:y1]])
+        assert here.min() > max(x[:x0].max() if x0 else -np.inf, y[:y0].max() if y0 else -np.inf)
+        for half in (0, 1):
+            bits = _merge_ref(x[x0:x1], y[y0:y1], half)
+            word = masks[t, half * 8:(half + 1) * 8]
+            got = [(int(word[k // 32]) >> (k % 32)) & 1 for k in range(len(bits))]
+            assert got == [int(b) for b in bits]
+
+
+def test_fexp_host_arithmetic():
+    """csrc/fexp.cuh's q_div is the IEEE quotient and fexp is within 1 ulp of libm exp."""
+    exe = "/tmp/finom_fexp_check"
+    src = os.path.join(ROOT, "tests", "fexp_check.cu")
+    r = subprocess.run(["nvcc", "-std=c++17", "-O2", "-w", "-o", exe, src], capture_output=True,
+                       text=True)
+    if r.returncode != 0:
+        pytest.skip("nvcc unavailable: " + r.stderr[-200:])
+    out = subprocess.run([exe, "1000000"], capture_output=True, text=True, check=True).stdout
+    n, badq, bade, maxulp = out.split()
+    assert int(badq) == 0
+    assert float(maxulp) <= 1.0
+    assert int(bade) < int(n) // 100
