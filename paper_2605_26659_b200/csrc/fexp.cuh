@@ -138,28 +138,37 @@ __device__ __noinline__ double fexp_slow(double x) { return exp(x); }
 inline double fexp_slow(double x) { return std::exp(x); }
 #endif
 
+// Polynomial / reduction constants: in constant memory on the device so the
+// DFMAs take them as c[] operands instead of materialising immediates.
+#define FB_EXP_CONSTS 0x1.71547652b82fep+6, 6755399441055744.0, 0x1.62e42fee00000p-7, \
+    0x1.a39ef35793c76p-39, 1.0 / 720, 1.0 / 120, 1.0 / 24, 1.0 / 6
+__device__ __constant__ double FB_EC[8] = {FB_EXP_CONSTS};
+static const double FB_EH[8] = {FB_EXP_CONSTS};
+#ifdef __CUDA_ARCH__
+#define FB_K(i) FB_EC[i]
+#else
+#define FB_K(i) FB_EH[i]
+#endif
+
 FB_HD double fexp(double x, const double2* __restrict__ tab) {
 #ifdef FB_DBG_NOEXP
   return 1.0 + x * 1e-30;  // timing experiment only: no exponential
 #endif
-  if (!(x > -707.0 && x < 709.0)) return fexp_slow(x);
-  const double L2E64 = 0x1.71547652b82fep+6;   // 64/ln2
-  const double LN2HI = 0x1.62e42fee00000p-7;   // ln2/64, 21 trailing zero bits
-  const double LN2LO = 0x1.a39ef35793c76p-39;
-  const double MAGIC = 6755399441055744.0;     // 1.5 * 2^52
-  double t = FB_FMA(x, L2E64, MAGIC);
-  double n = FB_SUB(t, MAGIC);
-  double r = FB_FMA(n, -LN2HI, x);
-  r = FB_FMA(n, -LN2LO, r);
-  double p = FB_FMA(r, 1.0 / 720, 1.0 / 120);
-  p = FB_FMA(p, r, 1.0 / 24);
-  p = FB_FMA(p, r, 1.0 / 6);
+  // fast path for |x| < 704 (high word compare; NaN/inf/large go out of line)
+  if ((unsigned)(fb_hi(x) & 0x7fffffff) >= 0x40860000u) return fexp_slow(x);
+  const double t = FB_FMA(x, FB_K(0), FB_K(1));   // x * 64/ln2 + 1.5*2^52
+  const double n = FB_SUB(t, FB_K(1));
+  double r = FB_FMA(n, -FB_K(2), x);
+  r = FB_FMA(n, -FB_K(3), r);
+  double p = FB_FMA(r, FB_K(4), FB_K(5));
+  p = FB_FMA(p, r, FB_K(6));
+  p = FB_FMA(p, r, FB_K(7));
   p = FB_FMA(p, r, 0.5);
   p = FB_FMA(p, r, 1.0);
   p = FB_MUL(p, r);
-  int ni = fb_lo(t);
-  double2 T = tab[ni & 63];
-  double res = FB_ADD(T.x, FB_FMA(T.x, p, T.y));
+  const int ni = fb_lo(t);
+  const double2 T = tab[ni & 63];
+  const double res = FB_ADD(T.x, FB_FMA(T.x, p, T.y));
   return fb_hilo(fb_hi(res) + ((ni >> 6) << 20), fb_lo(res));
 }
 

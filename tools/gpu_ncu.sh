@@ -1,5 +1,5 @@
 ITERS=${ITERS:-3}
 export ITERS
 python tools/ncu_target.py > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_half -s 2 -c 2 -o gpurun_out/prof_khalf2 python tools/ncu_target.py > gpurun_out/ncu2.log 2>&1; echo "ncu rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:k_step -s 2 -c 2 -o gpurun_out/prof_kstep python tools/ncu_target.py > gpurun_out/ncu2.log 2>&1; echo "ncu rc=$?"
 tail -2 gpurun_out/ncu2.log
