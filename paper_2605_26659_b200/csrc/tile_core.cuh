@@ -126,6 +126,86 @@ __device__ __forceinline__ double warp_min(double v) {
   return v;
 }
 
+// Lane-incoming states of one direction of a tile's recurrence.  f is the
+// lane's chunk map; (p_in, acc_in) enters lane 0 (UP, forward) or lane 31
+// (backward).  Two short scans replace one over 5-component maps: first the
+// column sums that cross lanes (a segmented sum of E, reset by lanes holding
+// a row: D == 0), then the affine recurrence p' = A p + (B acc + C) with
+// those sums folded in.
+template <bool UP>
+__device__ __forceinline__ void lane_states(const Tf &f, double p_in, double acc_in, double &p,
+                                            double &acc) {
+  const int lane = threadIdx.x & 31;
+  double E = f.E;
+  int D = f.D != 0.0;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double Eo = UP ? __shfl_up_sync(0xffffffffu, E, off) : __shfl_down_sync(0xffffffffu, E, off);
+    const int Do = UP ? __shfl_up_sync(0xffffffffu, D, off) : __shfl_down_sync(0xffffffffu, D, off);
+    if (UP ? lane >= off : lane + off < 32) {
+      if (D) E = __dadd_rn(Eo, E);
+      D &= Do;
+    }
+  }
+  double Ex = UP ? __shfl_up_sync(0xffffffffu, E, 1) : __shfl_down_sync(0xffffffffu, E, 1);
+  int Dx = UP ? __shfl_up_sync(0xffffffffu, D, 1) : __shfl_down_sync(0xffffffffu, D, 1);
+  if (UP ? lane == 0 : lane == 31) {
+    Ex = 0.0;
+    Dx = 1;
+  }
+  acc = Dx ? __dadd_rn(acc_in, Ex) : Ex;
+  double A = f.A, C = __fma_rn(f.B, acc, f.C);
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double Ao = UP ? __shfl_up_sync(0xffffffffu, A, off) : __shfl_down_sync(0xffffffffu, A, off);
+    const double Co = UP ? __shfl_up_sync(0xffffffffu, C, off) : __shfl_down_sync(0xffffffffu, C, off);
+    if (UP ? lane >= off : lane + off < 32) {
+      C = __fma_rn(A, Co, C);
+      A = __dmul_rn(A, Ao);
+    }
+  }
+  double Ax = UP ? __shfl_up_sync(0xffffffffu, A, 1) : __shfl_down_sync(0xffffffffu, A, 1);
+  double Cx = UP ? __shfl_up_sync(0xffffffffu, C, 1) : __shfl_down_sync(0xffffffffu, C, 1);
+  if (UP ? lane == 0 : lane == 31) {
+    Ax = 1.0;
+    Cx = 0.0;
+  }
+  p = __fma_rn(Ax, p_in, Cx);
+}
+
+// Max / min over the warp of non-negative doubles (no NaN): the IEEE bit
+// patterns order like the values, so two 32-bit warp reductions suffice.
+__device__ __forceinline__ double warp_max_pos(double v) {
+  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  return __hiloint2double((int)mh, (int)ml);
+}
+__device__ __forceinline__ double warp_min_pos(double v) {
+  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+  const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+  return __hiloint2double((int)mh, (int)ml);
+}
+
+// Warp sums of four quantities by reduce-scatter in a fixed order: on return
+// lane 0 holds the sum of q0, lane 8 of q1, lane 16 of q2, lane 24 of q3
+// (lanes 0-7, 8-15, ... hold the same value).
+__device__ __forceinline__ double warp_sum4(double q0, double q1, double q2, double q3) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8;
+  double k0 = b4 ? q2 : q0, k1 = b4 ? q3 : q1;
+  const double s0 = b4 ? q0 : q2, s1 = b4 ? q1 : q3;
+  k0 = __dadd_rn(k0, __shfl_xor_sync(0xffffffffu, s0, 16));
+  k1 = __dadd_rn(k1, __shfl_xor_sync(0xffffffffu, s1, 16));
+  double k = b3 ? k1 : k0;
+  const double s = b3 ? k0 : k1;
+  k = __dadd_rn(k, __shfl_xor_sync(0xffffffffu, s, 8));
+#pragma unroll
+  for (int off = 4; off > 0; off >>= 1) k = __dadd_rn(k, __shfl_xor_sync(0xffffffffu, k, off));
+  return k;
+}
+
 // ---------------------------------------------------------------------------
 // Wait-free carry resolution tree.  Level 0 nodes are tiles, level L+1 nodes
 // group FAN consecutive level-L nodes of one problem; the single level-3
@@ -152,11 +232,23 @@ __device__ __forceinline__ Tf ldcg_tf(const Tf *p) {
   return Tf{__ldcg(&p->A), __ldcg(&p->B), __ldcg(&p->C), __ldcg(&p->D), __ldcg(&p->E)};
 }
 
-// Called by a full warp after lane 0 wrote its tile node (maps + partials).
-// Returns true in the warp that completed the problem; then `top` holds the
+// Level-0 arrival of tile lt (lane 0 issues the release atomic on the parent
+// counter and gets its old value; the caller may do independent work before
+// handing it to tree_arrive_from).
+__device__ __forceinline__ int tree_arrive_begin(const Resolve &R, const TreeGeo &tg, int lt) {
+  int old = 0;
+  if ((threadIdx.x & 31) == 0) {
+    Node *pn = R.lev[1] + tg.base[1] + lt / FAN;
+    asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(&pn->cnt) : "memory");
+  }
+  return old;
+}
+
+// Continues an arrival whose level-0 atomic returned old0 (lane 0).  Returns
+// true in the warp that completed the problem; then `top` holds the
 // problem's reduced partials.
-__device__ __forceinline__ bool tree_arrive(const Resolve &R, const TreeGeo &tg, int lt,
-                                            double (&top)[4]) {
+__device__ __forceinline__ bool tree_arrive_from(const Resolve &R, const TreeGeo &tg, int lt,
+                                                 int old0, double (&top)[4]) {
   const int lane = threadIdx.x & 31;
   int idx = lt;
 #pragma unroll 1
@@ -166,9 +258,10 @@ __device__ __forceinline__ bool tree_arrive(const Resolve &R, const TreeGeo &tg,
     Node *pn = R.lev[L + 1] + tg.base[L + 1] + parent;
     int last = 0;
     if (lane == 0) {
-      int old;
-      asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;"
-                   : "=r"(old) : "l"(&pn->cnt) : "memory");
+      int old = old0;
+      if (L > 0)
+        asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(&pn->cnt) : "memory");
       last = old == nchild - 1;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
@@ -212,6 +305,12 @@ __device__ __forceinline__ bool tree_arrive(const Resolve &R, const TreeGeo &tg,
     idx = parent;
   }
   return true;
+}
+
+// Called by a full warp after lane 0 wrote its tile node (maps + partials).
+__device__ __forceinline__ bool tree_arrive(const Resolve &R, const TreeGeo &tg, int lt,
+                                            double (&top)[4]) {
+  return tree_arrive_from(R, tg, lt, tree_arrive_begin(R, tg, lt), top);
 }
 
 // Incoming forward state (from the left) and backward state (from the right)
