@@ -5,8 +5,8 @@ mangled = "_ZN2fb6k_stepILi%sEEEvNS_3DevE" % pick
 out = subprocess.run("TOP=100000 PICK='(int)%s' python tools/ncu_lines.py %s k_step %s" % (pick, rep, mangled),
                      shell=True, capture_output=True, text=True).stdout
 src = open("paper_2605_26659_b200/csrc/finom_1d.cu").read().splitlines()
-start = next(i for i, l in enumerate(src) if "k_step(Dev d) {" in l) + 1
-marks = [(i + 1, l.strip()) for i, l in enumerate(src[start:start + 400], start) if l.strip().startswith("// ----")]
+start = next(i for i, l in enumerate(src) if "void tile_compute(" in l) + 1
+marks = [(i + 1, l.strip()) for i, l in enumerate(src[start:start + 600], start) if l.strip().startswith("// ----")]
 def grp(f, l):
     if f == "finom_1d.cu":
         name = "k_step prologue"

@@ -16,8 +16,8 @@ iters = 10
 _lib.check(lib.finom_profile1d(bs.plan.handle, _lib.ptr(bs.u), _lib.ptr(bs.v), _lib.ptr(bs.phi), _lib.ptr(bs.psi), _lib.ptr(bs.a), _lib.ptr(bs.b), iters, 1, 200.0, _lib.ptr(hist), _lib.ptr(prof), _lib.stream_ptr()), "prof")
 lib.finom_phase_read(_lib.ptr(ph))
 T = bs.plan.info()["tiles"]
-names = ["wait/desc", "mask (RT2)", "col operands", "maps+scan+carry", "apply", "epilogue", "reduce+node"]
-tot = ph[:len(names)].sum()
+names = ["wait full", "mask", "col operands", "maps+carry+states", "apply", "epilogue", "reduce+node", "-", "P: desc batch", "P: wait empty", "P: issue"]
+tot = ph[:8].sum()
 for k, n in enumerate(names):
     print("%-14s %8.0f cycles/tile  %5.1f%%" % (n, ph[k] / (T * iters * 2), 100 * ph[k] / tot))
 print("halfA %.3f halfB %.3f ms" % (prof[0], prof[1]))
