@@ -316,10 +316,17 @@ def main():
                                    _lib.ptr(bs.b), itr, 1, 200.0, _lib.ptr(hist_dev),
                                    _lib.ptr(prof), _lib.stream_ptr()), "finom_profile1d")
     NX, NY = bs.u.numel(), bs.v.numel()
-    bytes_a = 8 * (4 * NY + 2 * NX)   # y, v, psi_old, psi_new | x, phi
-    bytes_b = 8 * (3 * NX + 2 * NY)   # x, u, phi_new | y, psi
+    # algorithmic bytes: per iteration 40n + 48m unabsorbed,
+    # 56n + 64m once the problem has absorbed (shift reads), weighted by the
+    # iterations each problem spends in either state in this solve
+    ns = np.array([x.size for x in wl["xs"]], dtype=np.float64)
+    ms_ = np.array([y.size for y in wl["ys"]], dtype=np.float64)
+    abs_its = bs.abs_its.view(bs.P, itr).cpu().numpy()
+    first = np.where(info[:, 3] > 0, abs_its[:, 0], itr).astype(np.float64)
+    alg_bytes_it = float(np.sum((40 * ns + 48 * ms_) * first
+                                + (56 * ns + 64 * ms_) * (itr - first))) / itr
     t_half = (prof[0] + prof[1]) * 1e-3
-    achieved = (bytes_a + bytes_b) / t_half / 1e9
+    achieved = alg_bytes_it / t_half / 1e9
     peak, peak_src = peaks()
     launches = int(lib.finom_solve1d_launches(bs.plan.handle, itr, 1)) * args.steps
 
@@ -364,11 +371,14 @@ def main():
             "data": "synthetic (seeded generators, BASELINE.json shapes; see DESIGN.md)",
             "config": config_json(cfg, wl, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic("k_half"),
+                         "frac": achieved / peak, "traffic": ncu_traffic("k_step"),
                          "peak_source": peak_src,
-                         "kernel": "k_half<A>+k_half<B> (88 B/pt-iteration algorithmic)",
-                         "ms_half_a": prof[0], "ms_half_b": prof[1], "ms_scan": prof[2],
-                         "ms_absorb": prof[3], "ms_iteration_ungraphed": prof[4]},
+                         "kernel": "k_step<A>+k_resolve<A>+k_step<B>+k_resolve<B>",
+                         "algorithmic_bytes_per_iteration": alg_bytes_it,
+                         "bytes_rule": "88 B/pt unabsorbed, 120 B/pt absorbed (SURVEY 8d)",
+                         "ms_half_a": prof[0], "ms_half_b": prof[1],
+                         "ms_resolve": prof[2], "ms_absorb": prof[3],
+                         "ms_iteration_ungraphed": prof[4]},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,

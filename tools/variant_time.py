@@ -13,4 +13,4 @@ prof = np.zeros(6)
 hist = torch.zeros(20, dtype=torch.float64, device="cuda")
 for rep in range(2):
     _lib.check(lib.finom_profile1d(bs.plan.handle, _lib.ptr(bs.u), _lib.ptr(bs.v), _lib.ptr(bs.phi), _lib.ptr(bs.psi), _lib.ptr(bs.a), _lib.ptr(bs.b), 10, 1, 200.0, _lib.ptr(hist), _lib.ptr(prof), _lib.stream_ptr()), "prof")
-print(os.path.basename(lib_path), "halfA %.3f halfB %.3f absorb %.3f ms" % (prof[0], prof[1], prof[3]))
+print(os.path.basename(lib_path), "halfA %.3f halfB %.3f (resolve %.3f) absorb %.3f ms" % (prof[0], prof[1], prof[2], prof[3]))
