@@ -135,8 +135,11 @@ def workload(cfg, rank=0, world=1):
     raise SystemExit("unknown config %r" % cfg)
 
 
-def run_2d(args, cfg, wl):
-    """2D configs (3: 1024^2, 4: 8192^2): finom_sinkhorn2d_host; value from its loop window."""
+def run_2d(args, cfg, wl, world=1, rank=0):
+    """2D configs (3: 1024^2, 4: 8192^2).  One GPU: sinkhorn_2d (value from its
+    loop window).  Under torchrun (world > 1): the row-sharded solve
+    (sharding.sinkhorn_2d_row_sharded, NCCL carry exchange), time = max over
+    ranks, total work fixed ("scaling": "strong")."""
     import paper_2605_26659_b200 as fb
     x1, y1, x2, y2, U, V = wl["grid"]
     src = fb.Grid2D(fb.Mesh1D(x1), fb.Mesh1D(y1))
@@ -144,23 +147,32 @@ def run_2d(args, cfg, wl):
     scfg = fb.SolverConfig(epsilon=wl["eps"][0], itr_max=wl["itr"], tol=0.0, stabilize=True)
     mu, mv = fb.Measure2D(U), fb.Measure2D(V)
     pts = x1.size * y1.size
+    if world > 1:
+        from paper_2605_26659_b200 import sharding as S
+        run = lambda: S.sinkhorn_2d_row_sharded(src, tgt, mu, mv, scfg)
+    else:
+        run = lambda: fb.sinkhorn_2d(src, tgt, mu, mv, scfg)
     for _ in range(max(1, min(args.warmup, 2))):
-        fb.sinkhorn_2d(src, tgt, mu, mv, scfg)
+        run()
     loops, walls = [], []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        sol = fb.sinkhorn_2d(src, tgt, mu, mv, scfg)
+        sol = run()
         walls.append(time.perf_counter() - t0)
         loops.append(sol.wall_time - sol.setup_time)
     loop = statistics.median(loops)
+    if rank != 0:
+        return
     line = {
-        "metric": METRIC, "value": pts * wl["itr"] / loop, "unit": UNIT, "n_gpus": 1,
+        "metric": METRIC, "value": pts * wl["itr"] / loop, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * loop,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, BASELINE.json shapes; see DESIGN.md)",
         "config": {"workload": "config%d: 2D %dx%d eps=%g %d it (stabilize=True)" % (
             cfg, x1.size, y1.size, wl["eps"][0], wl["itr"]), "itr_max": wl["itr"],
-            "timing": "loop window of sinkhorn_2d (host-driven loop, one sync per iteration)"},
+            "parallelism": "row shards x%d (carry exchange)" % world if world > 1 else "1 GPU",
+            "timing": "loop window (max over ranks); host-driven loop, one sync per iteration"},
         "e2e": {"value": pts * wl["itr"] / statistics.median(walls), "unit": UNIT,
                 "h2d_bytes_per_step": 8 * (2 * pts + 2 * x1.size + 2 * y1.size),
                 "d2h_bytes_per_step": 8 * 4 * pts},
@@ -263,8 +275,12 @@ def main():
     cfg = args.config
     wl = workload(cfg, rank, world)
     if cfg in (3, 4):
-        if rank == 0:
+        if cfg == 4 or world == 1:
+            run_2d(args, cfg, wl, world, rank)
+        elif rank == 0:
             run_2d(args, cfg, wl)
+        if world > 1:
+            torch.distributed.destroy_process_group()
         return
     itr = wl["itr"]
     bs = fb.BatchSolver1D(wl["xs"], wl["ys"], wl["us"], wl["vs"], wl["eps"])

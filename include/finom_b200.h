@@ -150,6 +150,29 @@ int finom_cost2d_host(int64_t n1, const double *x1, int64_t m1, const double *y1
                       const double *x2, int64_t m2, const double *y2, double eps, const double *A,
                       const double *B, const double *phi, const double *psi, double *cost);
 
+/* ---- Row-sharded 2D grids (no reference equivalent) ----
+ * One handle per rank for source == target grids x[n] x (y1[m1] | y2[m2]),
+ * rank holding grid rows [k0, k1).  The caller drives run_driver's loop
+ * and the collectives (paper_2605_26659_b200.sharding.sinkhorn_2d_row_sharded):
+ * per half, finom_grid2d_xpre writes this shard's segment totals of the x
+ * sweep (10 doubles per line), the caller all-gathers them ([R][line][10]),
+ * finom_grid2d_finish completes the half and writes the shard's partials
+ * (err, max, min, failure code) for an all-reduce.  Local grids are
+ * column-major (k1 - k0) x m. */
+typedef struct finom_grid2d finom_grid2d;
+int finom_grid2d_create(int64_t n, const double *x, int64_t m1, const double *y1, int64_t m2,
+                        const double *y2, double eps, int64_t k0, int64_t k1, finom_grid2d **out);
+int finom_grid2d_destroy(finom_grid2d *g);
+int finom_grid2d_set_shifts(finom_grid2d *g, const double *A, const double *B, void *stream);
+int finom_grid2d_xpre(finom_grid2d *g, int half, const double *in, const double *shift, int dyn,
+                      double *seg_out, void *stream);
+int finom_grid2d_finish(finom_grid2d *g, int half, const double *in, const double *A,
+                        const double *B, int dyn, const double *seg_all, int R, int r,
+                        const double *W, double *SC, double *part_out, void *stream);
+int finom_grid2d_absorb(finom_grid2d *g, int side, double *shift, const double *W,
+                        const double *SC_all, const int32_t *prv, const int32_t *nxt, int R, int r,
+                        void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,15 @@ SIGNATURES = {
                                     _vp, _vp, _vp, _c_int, _vp]),
     "finom_cost2d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl,
                                    _vp, _vp, _vp, _vp, _vp]),
+    "finom_grid2d_create": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_i64,
+                                     _c_i64, _vp]),
+    "finom_grid2d_destroy": (_c_int, [_vp]),
+    "finom_grid2d_set_shifts": (_c_int, [_vp, _vp, _vp, _vp]),
+    "finom_grid2d_xpre": (_c_int, [_vp, _c_int, _vp, _vp, _c_int, _vp, _vp]),
+    "finom_grid2d_finish": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int,
+                                     _vp, _vp, _vp, _vp]),
+    "finom_grid2d_absorb": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                                     _vp]),
 }
 
 _lib = None

@@ -315,9 +315,18 @@ __device__ __forceinline__ bool tree_arrive(const Resolve &R, const TreeGeo &tg,
 
 // Incoming forward state (from the left) and backward state (from the right)
 // of tile lt of a problem.
+// init (nullable): per problem incoming states (p, acc, q, accb) of the
+// problem's first / last tile (a row shard's carries from the other shards).
 __device__ __forceinline__ void tree_carry(const Resolve &R, const TreeGeo &tg, int lt, double &p,
-                                           double &acc, double &q, double &accb) {
+                                           double &acc, double &q, double &accb,
+                                           const double *init = nullptr, int prob = 0) {
   p = acc = q = accb = 0.0;
+  if (init) {
+    p = init[4 * prob];
+    acc = init[4 * prob + 1];
+    q = init[4 * prob + 2];
+    accb = init[4 * prob + 3];
+  }
   int id[NLEV - 1];
   id[0] = lt;
   for (int L = 1; L < NLEV - 1; ++L) id[L] = id[L - 1] / FAN;
@@ -393,15 +402,17 @@ __device__ __forceinline__ void load_halo_async(double *dst, const double *src, 
 }
 
 // dst[-1 .. cnt] <- src[lo-1 .. lo+cnt] (halo entries only where they exist)
+// (indices outside [w0, N) read as 0: mesh ends, or the edges of a row
+// shard's data window)
 __device__ __forceinline__ void load_halo(double *dst, const double *src, int lo, int cnt, int N,
-                                          bool zero) {
+                                          bool zero, int w0 = 0) {
   const int lane = threadIdx.x & 31;
   if (zero) {
     for (int k = lane - 1; k <= cnt; k += 32) dst[k] = 0.0;
     return;
   }
   for (int k = lane; k < cnt; k += 32) dst[k] = __ldg(src + lo + k);
-  if (lane == 0) dst[-1] = lo > 0 ? __ldg(src + lo - 1) : 0.0;
+  if (lane == 0) dst[-1] = lo > w0 ? __ldg(src + lo - 1) : 0.0;
   if (lane == 1) dst[cnt] = lo + cnt < N ? __ldg(src + lo + cnt) : 0.0;
 }
 

@@ -71,3 +71,270 @@ def max_over_ranks(seconds):
         t = t.cuda()
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# Row-sharded 2D grids (BASELINE config 4).
+#
+# Rank r holds grid rows [k0, k1) (x index) of source == target grids.  The
+# y sweeps are local; the x sweep of every half needs the other shards'
+# carries: each shard resolves its segment of every column line on the
+# device, the segment totals (10 doubles per line) are all-gathered, and the
+# shard composes the totals of the shards before / after it into each line's
+# incoming state (finom_grid2d_xpre / finom_grid2d_finish).  The reductions
+# of the epilogue (marginal error, extremes, failure) are all-reduced, and
+# run_driver's decisions (solver.py:173-198) are taken identically on every
+# rank.  An absorption all-gathers the scalings once (np.interp over the flat
+# index of the whole grid may reach into another shard).
+
+
+def grid_row_ranges(n, world):
+    """Row shards [k0, k1) of an n-row grid (equal sizes: n % world == 0)."""
+    if n % world:
+        raise ValueError("row-sharded grids need n divisible by the world size")
+    nl = n // world
+    return [(r * nl, (r + 1) * nl) for r in range(world)]
+
+
+def to_shard(flat, n, m, k0, k1):
+    """Rows [k0, k1) of a column-major n x m grid, column-major (k1-k0) x m."""
+    return np.ascontiguousarray(np.asarray(flat).reshape(m, n)[:, k0:k1]).ravel()
+
+
+def from_shards(parts, n, m, ranges):
+    """Reassemble column-major shards into the flat column-major n x m grid."""
+    g = np.empty((m, n))
+    for part, (k0, k1) in zip(parts, ranges):
+        g[:, k0:k1] = np.asarray(part).reshape(m, k1 - k0)
+    return g.ravel()
+
+
+def _pos_index(w):
+    """Previous / next positive-mass flat index (solver._shift's np.interp support)."""
+    idx = np.arange(w.size)
+    pos = w > 0
+    prv = np.maximum.accumulate(np.where(pos, idx, -1))
+    nxt = np.minimum.accumulate(np.where(pos, idx, w.size)[::-1])[::-1]
+    return prv.astype(np.int32), nxt.astype(np.int32)
+
+
+class RowShard2D:
+    """One rank's state of a row-sharded 2D solve (device buffers + C handle)."""
+
+    def __init__(self, x, y1, y2, U, V, eps, k0, k1):
+        import ctypes
+        import torch
+        from . import _lib
+        self.lib = _lib.load()
+        self._lib = _lib
+        n, m1, m2 = len(x), len(y1), len(y2)
+        self.n, self.m1, self.m2, self.k0, self.k1, self.eps = n, m1, m2, k0, k1, eps
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.finom_grid2d_create(n, _lib.ptr(x), m1, _lib.ptr(y1), m2,
+                                                _lib.ptr(y2), float(eps), k0, k1,
+                                                ctypes.byref(h)), "finom_grid2d_create")
+        self.h = h
+        dev = torch.device("cuda")
+        f64 = dict(dtype=torch.float64, device=dev)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+        self.U = t(to_shard(U, n, m1, k0, k1))
+        self.V = t(to_shard(V, n, m2, k0, k1))
+        self.PHI = torch.full(((k1 - k0) * m1,), 1.0 / (n * m1), **f64)
+        self.PSI = torch.full(((k1 - k0) * m2,), 1.0 / (n * m1), **f64)
+        self.A = torch.zeros((k1 - k0) * m1, **f64)
+        self.B = torch.zeros((k1 - k0) * m2, **f64)
+        self.seg = torch.empty(10 * max(m1, m2), **f64)
+        self.part = torch.empty(4, **f64)
+        pu, nu = _pos_index(np.asarray(U))
+        pv, nv = _pos_index(np.asarray(V))
+        ti = lambda a: torch.from_numpy(a).to(dev)
+        self.prvU, self.nxtU, self.prvV, self.nxtV = ti(pu), ti(nu), ti(pv), ti(nv)
+
+    def close(self):
+        if self.h:
+            self.lib.finom_grid2d_destroy(self.h)
+            self.h = None
+
+    def lines(self, half):
+        return self.m1 if half == 0 else self.m2
+
+    def xpre(self, half, dyn):
+        L, P = self._lib, self._lib.ptr
+        inp, sh = (self.PHI, self.A) if half == 0 else (self.PSI, self.B)
+        L.check(self.lib.finom_grid2d_xpre(self.h, half, P(inp), P(sh), int(dyn), P(self.seg),
+                                           L.stream_ptr()), "finom_grid2d_xpre")
+        return self.seg[:10 * self.lines(half)]
+
+    def finish(self, half, dyn, seg_all, R, r):
+        L, P = self._lib, self._lib.ptr
+        inp, W, SC = (self.PHI, self.V, self.PSI) if half == 0 else (self.PSI, self.U, self.PHI)
+        L.check(self.lib.finom_grid2d_finish(self.h, half, P(inp), P(self.A), P(self.B), int(dyn),
+                                             P(seg_all), R, r, P(W), P(SC), P(self.part),
+                                             L.stream_ptr()), "finom_grid2d_finish")
+        return self.part
+
+    def absorb(self, side, sc_all, R, r):
+        L, P = self._lib, self._lib.ptr
+        sh, W = (self.A, self.U) if side == 0 else (self.B, self.V)
+        prv, nxt = (self.prvU, self.nxtU) if side == 0 else (self.prvV, self.nxtV)
+        L.check(self.lib.finom_grid2d_absorb(self.h, side, P(sh), P(W), P(sc_all), P(prv), P(nxt),
+                                             R, r, L.stream_ptr()), "finom_grid2d_absorb")
+
+    def refresh_shifts(self):
+        L, P = self._lib, self._lib.ptr
+        L.check(self.lib.finom_grid2d_set_shifts(self.h, P(self.A), P(self.B), L.stream_ptr()),
+                "finom_grid2d_set_shifts")
+
+
+def combine_parts(parts):
+    """All-reduce of per-shard epilogue partials (err, max, min, failure code)."""
+    parts = np.asarray(parts, dtype=np.float64).reshape(-1, 4)
+    fails = parts[:, 3][parts[:, 3] >= 0]
+    return (float(np.sum(parts[:, 0])), float(np.max(parts[:, 1])), float(np.min(parts[:, 2])),
+            float(np.min(fails)) if fails.size else -1.0)
+
+
+def run_driver_2d(phase, absorb, config):
+    """run_driver (solver.py:156-199) over a sharded 2D iteration: phase(half,
+    dyn) returns the combined partials, absorb() performs _shift + absorb on
+    every shard.  Returns (iterations, converged, status, hist, absorb_its)."""
+    import math
+    hi, lo = math.exp(config.absorb_threshold), math.exp(-config.absorb_threshold)
+    it, dyn, status, converged = 0, False, 0, False
+    hist, abs_its = [], []
+    while it < config.itr_max:
+        pa = phase(0, dyn)
+        pb = phase(1, dyn)
+        it += 1
+        hist.append(pa[0])
+        if pa[3] >= 0 or pb[3] >= 0:
+            f = pa[3] if pa[3] >= 0 else pb[3]
+            status = int(f) & 3
+            break
+        if config.tol > 0 and pa[0] <= config.tol:
+            converged = True
+            break
+        if config.stabilize and (pb[1] > hi or pa[1] > hi or pb[2] < lo or pa[2] < lo):
+            absorb()
+            abs_its.append(it)
+            dyn = True
+    return it, converged, status, hist, abs_its
+
+
+def _solution_2d(source, target, config, phi, psi, A, B, it, conv, status, hist, abs_its,
+                 wall):
+    import dataclasses
+    from .kernel2d import KernelOperator2D, build_operator_2d, transport_cost_fast_2d
+    from .solver import Solution, history_from, raise_status
+    raise_status(status)
+    (n1, m1), (n2, m2) = source.shape, target.shape
+    op = build_operator_2d(source, target, config.epsilon)
+    op = KernelOperator2D(op.kx, op.ky, op.epsilon, A.reshape((n1, m1), order="F"),
+                          B.reshape((n2, m2), order="F"))
+    h = np.zeros(config.itr_max)
+    h[:len(hist)] = hist
+    sol = Solution(phi=phi, psi=psi, a=A, b=B, kernel=op, iterations_run=it, converged=conv,
+                   marginal_error_history=history_from(h, it, conv, config), wall_time=wall,
+                   setup_time=0.0, cost=float("nan"), config=config,
+                   absorb_iterations=list(abs_its))
+    return dataclasses.replace(sol, cost=float(transport_cost_fast_2d(sol)))
+
+
+def _check_grids(source, target):
+    from .errors import ConfigError
+    x1, x2 = source.x_nodes.nodes, target.x_nodes.nodes
+    if len(x1) != len(x2) or not np.array_equal(x1, x2):
+        raise ConfigError("row sharding needs source and target grids with the same x nodes")
+
+
+def sinkhorn_2d_row_sharded(source, target, u, v, config, group=None):
+    """sinkhorn_2d with the grid rows sharded over the process group (one GPU
+    per rank, NCCL).  Every rank passes the whole problem; returns the
+    Solution (gathered) on every rank."""
+    import time
+    import torch
+    import torch.distributed as dist
+    _check_grids(source, target)
+    R, r = dist.get_world_size(group), dist.get_rank(group)
+    n, m1, m2 = source.shape[0], source.shape[1], target.shape[1]
+    ranges = grid_row_ranges(n, R)
+    k0, k1 = ranges[r]
+    U = u.weights.ravel(order="F")
+    V = v.weights.ravel(order="F")
+    sh = RowShard2D(source.x_nodes.nodes, source.y_nodes.nodes, target.y_nodes.nodes, U, V,
+                    config.epsilon, k0, k1)
+    dev = sh.PHI.device
+    seg_all = {h: torch.empty(R * 10 * sh.lines(h), dtype=torch.float64, device=dev)
+               for h in (0, 1)}
+    parts = torch.empty(4 * R, dtype=torch.float64, device=dev)
+
+    def phase(half, dyn):
+        seg = sh.xpre(half, dyn)
+        dist.all_gather_into_tensor(seg_all[half], seg.contiguous(), group=group)
+        part = sh.finish(half, dyn, seg_all[half], R, r)
+        dist.all_gather_into_tensor(parts, part, group=group)
+        return combine_parts(parts.cpu().numpy())
+
+    def absorb():
+        for side, sc in ((0, sh.PHI), (1, sh.PSI)):
+            sc_all = torch.empty(R * sc.numel(), dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(sc_all, sc, group=group)
+            sh.absorb(side, sc_all, R, r)
+        sh.PHI.fill_(1.0)
+        sh.PSI.fill_(1.0)
+        sh.refresh_shifts()
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    it, conv, status, hist, abs_its = run_driver_2d(phase, absorb, config)
+    torch.cuda.synchronize()
+    wall = max_over_ranks(time.perf_counter() - t0)
+    out = {}
+    for name, t in (("phi", sh.PHI), ("psi", sh.PSI), ("A", sh.A), ("B", sh.B)):
+        g = torch.empty(R * t.numel(), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(g, t, group=group)
+        m = m1 if name in ("phi", "A") else m2
+        out[name] = from_shards(np.split(g.cpu().numpy(), R), n, m, ranges)
+    sh.close()
+    return _solution_2d(source, target, config, out["phi"], out["psi"], out["A"], out["B"], it,
+                        conv, status, hist, abs_its, wall)
+
+
+def sinkhorn_2d_row_sharded_sim(source, target, u, v, config, R):
+    """The row-sharded algorithm with R shards in ONE process on one GPU: the
+    shards' phases run one after another and the collectives are plain
+    concatenations (a correctness check of the decomposition; never a
+    timing)."""
+    import torch
+    _check_grids(source, target)
+    n, m1, m2 = source.shape[0], source.shape[1], target.shape[1]
+    ranges = grid_row_ranges(n, R)
+    U = u.weights.ravel(order="F")
+    V = v.weights.ravel(order="F")
+    shards = [RowShard2D(source.x_nodes.nodes, source.y_nodes.nodes, target.y_nodes.nodes, U, V,
+                         config.epsilon, k0, k1) for k0, k1 in ranges]
+
+    def phase(half, dyn):
+        seg_all = torch.cat([s.xpre(half, dyn).clone() for s in shards])
+        parts = [s.finish(half, dyn, seg_all, R, k).cpu().numpy() for k, s in enumerate(shards)]
+        return combine_parts(parts)
+
+    def absorb():
+        for side in (0, 1):
+            sc_all = torch.cat([(s.PHI if side == 0 else s.PSI) for s in shards])
+            for k, s in enumerate(shards):
+                s.absorb(side, sc_all, R, k)
+        for s in shards:
+            s.PHI.fill_(1.0)
+            s.PSI.fill_(1.0)
+            s.refresh_shifts()
+
+    it, conv, status, hist, abs_its = run_driver_2d(phase, absorb, config)
+    torch.cuda.synchronize()
+    out = {name: from_shards([getattr(s, name).cpu().numpy() for s in shards], n,
+                             m1 if name in ("PHI", "A") else m2, ranges)
+           for name in ("PHI", "PSI", "A", "B")}
+    for s in shards:
+        s.close()
+    return _solution_2d(source, target, config, out["PHI"], out["PSI"], out["A"], out["B"], it,
+                        conv, status, hist, abs_its, 0.0)

@@ -77,3 +77,53 @@ def test_config3_full_vs_reference_pins():
     print("config3 full parity", q)
     assert list(sol.absorb_iterations) == [int(t) for t in g["absorb_its"]]
     assert q["hist"] < 1 and q["phi"] < TOL and q["psi"] < TOL and q["cost"] < TOL, q
+
+
+def _sharded_case(n, m1, m2, eps, itr, seed, zero_rows=False, thr=200.0):
+    rng = np.random.default_rng(seed)
+    x = W.gap_mesh(rng, n, 0.1, 1.9)
+    y1 = W.gap_mesh(rng, m1, 0.1, 1.9)
+    y2 = W.gap_mesh(rng, m2, 0.1, 1.9)
+    U = W.blobs(x, y1, rng, 8)
+    V = W.blobs(x, y2, rng, 8)
+    if zero_rows:  # zero-mass stretches across the shard boundaries (np.interp fill)
+        U[n // 2 - 3:n // 2 + 4, :] = 0.0
+        V[n // 4 - 2:n // 4 + 3, : m2 // 2] = 0.0
+    U /= U.sum()
+    V /= V.sum()
+    cfg = fb.SolverConfig(epsilon=eps, itr_max=itr, tol=0.0, stabilize=True,
+                          absorb_threshold=thr)
+    return x, y1, y2, U, V, cfg
+
+
+@pytest.mark.parametrize("R,zero,thr,m2", [(2, False, 200.0, 40), (3, True, 30.0, 40),
+                                           (4, False, 30.0, 52)])
+def test_row_sharded_2d_vs_oracle(R, zero, thr, m2):
+    """SURVEY 8(e) config-4 decomposition: R row shards with carry exchange
+    (run one after another on one GPU, collectives as concatenation) against
+    the oracle of the unsharded reference algorithm."""
+    from oracle import oracle as O
+    from paper_2605_26659_b200 import sharding as S
+    x, y1, y2, U, V, cfg = _sharded_case(96, 40, m2, 2e-3, 50, 11 + R, zero, thr)
+    src, tgt = _grid(x, y1), _grid(x.copy(), y2)
+    sol = S.sinkhorn_2d_row_sharded_sim(src, tgt, fb.Measure2D(U), fb.Measure2D(V), cfg, R)
+    r = O.sinkhorn_2d(x, y1, x, y2, U, V, cfg.epsilon, cfg.itr_max, 0.0, True, thr)
+    assert r["status"] == 0
+    assert sol.iterations_run == r["iterations"]
+    assert list(sol.absorb_iterations) == list(r["absorb_its"])
+    assert len(r["absorb_its"]) > 0  # the absorbed (dyn) path is exercised
+    for key in ("phi", "psi", "a", "b"):
+        assert rel_inf(getattr(sol, key), r[key]) < TOL, key
+    assert abs(sol.cost - r["cost"]) <= TOL * abs(r["cost"])
+    hist = np.array([h[1] for h in sol.marginal_error_history])
+    assert np.allclose(hist, r["hist"], rtol=TOL, atol=1e-12)
+
+
+def test_row_sharded_2d_matches_single_gpu():
+    from paper_2605_26659_b200 import sharding as S
+    x, y1, y2, U, V, cfg = _sharded_case(64, 48, 48, 5e-3, 30, 7)
+    src, tgt = _grid(x, y1), _grid(x.copy(), y2)
+    a = S.sinkhorn_2d_row_sharded_sim(src, tgt, fb.Measure2D(U), fb.Measure2D(V), cfg, 4)
+    b = fb.sinkhorn_2d(src, tgt, fb.Measure2D(U), fb.Measure2D(V), cfg)
+    for key in ("phi", "psi", "a", "b"):
+        assert rel_inf(getattr(a, key), getattr(b, key)) < 1e-11, key

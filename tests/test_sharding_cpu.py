@@ -81,3 +81,89 @@ def test_sharded_batch_gloo_world2():
     assert costs == [r["cost"] for r in ref]
     assert all(np.array_equal(a, r["phi"]) for a, r in zip(phis, ref))
     assert t == 1.5
+
+
+def test_row_shard_layout_roundtrip():
+    from paper_2605_26659_b200 import sharding as S
+    n, m = 12, 5
+    g = np.arange(n * m, dtype=np.float64)
+    for R in (1, 2, 3, 4):
+        ranges = S.grid_row_ranges(n, R)
+        parts = [S.to_shard(g, n, m, k0, k1) for k0, k1 in ranges]
+        assert np.array_equal(S.from_shards(parts, n, m, ranges), g)
+        # local element (kl, l) is global (k0 + kl, l)
+        k0, k1 = ranges[-1]
+        assert parts[-1][1 + (k1 - k0) * 2] == g[k0 + 1 + n * 2]
+    with pytest.raises(ValueError):
+        S.grid_row_ranges(10, 3)
+
+
+def test_combine_parts_and_driver_logic():
+    from paper_2605_26659_b200 import sharding as S
+    from paper_2605_26659_b200 import SolverConfig
+    p = S.combine_parts([[1.0, 2.0, 0.5, -1.0], [2.0, 3.0, 0.25, 9.0], [0.5, 1.0, 0.75, 5.0]])
+    assert p == (3.5, 3.0, 0.25, 5.0)
+    assert S.combine_parts([[1.0, 2.0, 0.5, -1.0]])[3] == -1.0
+    # scripted phases: absorb trigger at iteration 2, failure (code 4 * 7 + 2) at 4
+    script = {(1, 0): (1.0, 1.0, 1.0, -1.0), (1, 1): (0.0, 1.0, 1.0, -1.0),
+              (2, 0): (0.5, 1e90, 1.0, -1.0), (2, 1): (0.0, 1.0, 1.0, -1.0),
+              (3, 0): (0.25, 1.0, 1.0, -1.0), (3, 1): (0.0, 1.0, 1.0, -1.0),
+              (4, 0): (0.1, 1.0, 1.0, 30.0), (4, 1): (0.0, 1.0, 1.0, -1.0)}
+    state = {"it": 1, "absorbs": 0}
+
+    def phase(half, dyn):
+        out = script[(state["it"], half)]
+        if half == 1:
+            state["it"] += 1
+        return out
+
+    def absorb():
+        state["absorbs"] += 1
+
+    cfg = SolverConfig(epsilon=1e-2, itr_max=10, stabilize=True, absorb_threshold=200.0)
+    it, conv, status, hist, abs_its = S.run_driver_2d(phase, absorb, cfg)
+    assert (it, conv, status) == (4, False, 2)
+    assert abs_its == [2] and state["absorbs"] == 1
+    assert hist == [1.0, 0.5, 0.25, 0.1]
+
+
+def _gather_shards_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_26659_b200 import sharding as S
+    dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % port, rank=rank,
+                            world_size=world)
+    n, m = 8, 3
+    g = np.arange(n * m, dtype=np.float64) * 0.5
+    ranges = S.grid_row_ranges(n, world)
+    mine = torch.from_numpy(S.to_shard(g, n, m, *ranges[rank]))
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    full = S.from_shards([p.numpy() for p in parts], n, m, ranges)
+    # the partial reduction of the sharded epilogue
+    part = torch.tensor([float(rank + 1), float(rank), 1.0 / (rank + 1), -1.0 if rank else 6.0],
+                        dtype=torch.float64)
+    allp = [torch.empty_like(part) for _ in range(world)]
+    dist.all_gather(allp, part)
+    q.put((rank, bool(np.array_equal(full, g)), S.combine_parts([p.numpy() for p in allp])))
+    dist.destroy_process_group()
+
+
+def test_row_shard_gather_gloo_world2():
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_gather_shards_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, ok, comb in res:
+        assert ok
+        assert comb == (3.0, 1.0, 0.5, 6.0)
