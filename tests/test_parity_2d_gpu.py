@@ -127,3 +127,31 @@ def test_row_sharded_2d_matches_single_gpu():
     b = fb.sinkhorn_2d(src, tgt, fb.Measure2D(U), fb.Measure2D(V), cfg)
     for key in ("phi", "psi", "a", "b"):
         assert rel_inf(getattr(a, key), getattr(b, key)) < 1e-11, key
+
+
+def test_row_sharded_2d_nccl_world1():
+    """The torch.distributed driver itself (NCCL collectives, one rank)."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2605_26659_b200 import sharding as S
+    x, y1, y2, U, V, cfg = _sharded_case(64, 40, 40, 2e-3, 25, 5, thr=30.0)
+    src, tgt = _grid(x, y1), _grid(x.copy(), y2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % port, rank=0,
+                                world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        a = S.sinkhorn_2d_row_sharded(src, tgt, fb.Measure2D(U), fb.Measure2D(V), cfg)
+    finally:
+        if own:
+            dist.destroy_process_group()
+    b = fb.sinkhorn_2d(src, tgt, fb.Measure2D(U), fb.Measure2D(V), cfg)
+    assert a.absorb_iterations == b.absorb_iterations
+    for key in ("phi", "psi", "a", "b"):
+        assert rel_inf(getattr(a, key), getattr(b, key)) < 1e-11, key
+    assert abs(a.cost - b.cost) <= 1e-11 * abs(b.cost)
