@@ -256,12 +256,13 @@ __device__ __forceinline__ int tree_arrive_begin(const Resolve &R, const TreeGeo
 // Continues an arrival whose level-0 atomic returned old0 (lane 0).  Returns
 // true in the warp that completed the problem; then `top` holds the
 // problem's reduced partials.
+// (L0 > 0: continue from level L0, lt then indexes that level's nodes)
 __device__ __forceinline__ bool tree_arrive_from(const Resolve &R, const TreeGeo &tg, int lt,
-                                                 int old0, double (&top)[4]) {
+                                                 int old0, double (&top)[4], int L0 = 0) {
   const int lane = threadIdx.x & 31;
   int idx = lt;
 #pragma unroll 1
-  for (int L = 0; L + 1 < NLEV; ++L) {
+  for (int L = L0; L + 1 < NLEV; ++L) {
     const int parent = idx / FAN;
     const int nchild = min(FAN, tg.n[L] - parent * FAN);
     Node *pn = R.lev[L + 1] + tg.base[L + 1] + parent;
@@ -269,13 +270,20 @@ __device__ __forceinline__ bool tree_arrive_from(const Resolve &R, const TreeGeo
     if (lane == 0) {
       int old = old0;
       if (L > 0)
+#ifdef FB_ACQREL
+        asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(&pn->cnt) : "memory");
+#else
         asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;"
                      : "=r"(old) : "l"(&pn->cnt) : "memory");
+#endif
       last = old == nchild - 1;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) return false;
+#ifndef FB_ACQREL
     __threadfence();
+#endif
     Node *ch = R.lev[L] + tg.base[L] + parent * FAN;
     const bool have = lane < nchild;
     Tf f = tf_id(), b = tf_id();
