@@ -387,7 +387,8 @@ def main():
             "data": "synthetic (seeded generators, BASELINE.json shapes; see DESIGN.md)",
             "config": config_json(cfg, wl, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic("k_step"),
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic("k_step") if cfg == 2 else None,
                          "peak_source": peak_src,
                          "kernel": "k_step<A>+k_resolve<A>+k_step<B>+k_resolve<B>",
                          "algorithmic_bytes_per_iteration": alg_bytes_it,
