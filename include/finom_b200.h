@@ -127,16 +127,18 @@ int finom_sinkhorn1d_host(int64_t n, const double *x, int64_t m, const double *y
 
 /* 2D grids (kernel2d.py:363-391 sinkhorn_2d with transport_cost_fast_2d).
  * Source grid x1[n1] x y1[m1], target x2[n2] x y2[m2]; U (n1 x m1) and V
- * (n2 x m2) column-major (x fastest, mesh.py:85-107).  Outputs phi, A
- * (n1*m1), psi, B (n2*m2) flat column-major; hist / info / absorb_its /
- * cost / timing as finom_sinkhorn1d_host.  Replaces _kernels.iter_2d_baked /
- * iter_2d_dyn (_kernels.py:353-521) driven by run_driver. */
+ * (n2 x m2) column-major (x fastest, mesh.py:85-107), or row-major when
+ * w_rowmajor != 0 (a C-ordered numpy grid; transposed on the device).
+ * Outputs phi, A (n1*m1), psi, B (n2*m2) flat column-major; hist / info /
+ * absorb_its / cost / timing as finom_sinkhorn1d_host.  Replaces
+ * _kernels.iter_2d_baked / iter_2d_dyn (_kernels.py:353-521) driven by
+ * run_driver. */
 int finom_sinkhorn2d_host(int64_t n1, const double *x1, int64_t m1, const double *y1, int64_t n2,
                           const double *x2, int64_t m2, const double *y2, const double *U,
                           const double *V, double eps, int64_t itr_max, double tol, int stabilize,
                           double absorb_threshold, double *phi, double *psi, double *A_out,
                           double *B_out, double *hist, int64_t *info, int64_t *absorb_its,
-                          double *cost, double *timing);
+                          double *cost, double *timing, int w_rowmajor);
 
 /* KernelOperator2D.apply (transpose = 0: out n1*m1 = K' in, in n2*m2) and
  * apply_transpose (transpose = 1) with optional shift grids A, B

@@ -41,7 +41,7 @@ SIGNATURES = {
                                        _vp, _vp, _vp]),
     "finom_sinkhorn2d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _vp,
                                        _vp, _c_dbl, _c_i64, _c_dbl, _c_int, _c_dbl, _vp, _vp,
-                                       _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+                                       _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int]),
     "finom_apply2d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl,
                                     _vp, _vp, _vp, _c_int, _vp]),
     "finom_cost2d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl,

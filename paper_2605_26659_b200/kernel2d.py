@@ -134,8 +134,17 @@ def sinkhorn_2d(source, target, u, v, config):
     (n1, m1), (n2, m2) = source.shape, target.shape
     x1, y1 = source.x_nodes.nodes, source.y_nodes.nodes
     x2, y2 = target.x_nodes.nodes, target.y_nodes.nodes
-    U = np.ascontiguousarray(u.weights.ravel(order="F"))
-    V = np.ascontiguousarray(v.weights.ravel(order="F"))
+    # a C-ordered grid goes as is (the library transposes it on the device;
+    # numpy's strided F-order ravel of a 512 MB grid costs over a second)
+    def weights_arg(w):
+        if w.flags.f_contiguous:
+            return np.asarray(w, dtype=np.float64).ravel(order="F"), 0
+        return np.ascontiguousarray(w, dtype=np.float64), 1
+    U, u_rm = weights_arg(u.weights)
+    V, v_rm = weights_arg(v.weights)
+    if u_rm != v_rm:  # mixed layouts: both flat column-major
+        U, u_rm = np.ascontiguousarray(u.weights.ravel(order="F")), 0
+        V = np.ascontiguousarray(v.weights.ravel(order="F"))
     itr = int(config.itr_max)
     phi, A = np.empty(n1 * m1), np.empty(n1 * m1)
     psi, B = np.empty(n2 * m2), np.empty(n2 * m2)
@@ -149,8 +158,8 @@ def sinkhorn_2d(source, target, u, v, config):
         n1, _lib.ptr(x1), m1, _lib.ptr(y1), n2, _lib.ptr(x2), m2, _lib.ptr(y2), _lib.ptr(U),
         _lib.ptr(V), config.epsilon, itr, float(config.tol), int(bool(config.stabilize)),
         float(config.absorb_threshold), _lib.ptr(phi), _lib.ptr(psi), _lib.ptr(A), _lib.ptr(B),
-        _lib.ptr(hist), _lib.ptr(info), _lib.ptr(abs_its), _lib.ptr(cost), _lib.ptr(timing)),
-        "finom_sinkhorn2d_host")
+        _lib.ptr(hist), _lib.ptr(info), _lib.ptr(abs_its), _lib.ptr(cost), _lib.ptr(timing),
+        u_rm), "finom_sinkhorn2d_host")
     raise_status(status)
     its, conv = int(info[0]), bool(info[1])
     op = build_operator_2d(source, target, config.epsilon)
