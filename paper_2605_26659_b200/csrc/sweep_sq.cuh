@@ -1,0 +1,255 @@
+// Square line sweeps: the 2D sweeps when a grid axis of the source equals
+// the target's (BASELINE configs 3 and 4: source grid == target grid).
+//
+// On such a line every mesh point z_r is both a row and a column, so the
+// merged order of kernel1d's dividing index (searchsorted "right",
+// kernel1d.py:55-62: the tie column r belongs to row r's lower block) is
+// fixed and the two recurrences of _dp_apply / _dp_apply_dyn
+// (_kernels.py:53-203) take one step per point instead of one per slot:
+//
+//   P_r = rho_r * P_{r-1} + delta_r * v_r        (lower block, columns <= r)
+//   Q_r = sigma_r * Q_{r+1} + mu_r * v_{r+1}     (upper block, columns > r)
+//   out_r = P_r + Q_r
+//
+// with, for row-side shifts alpha and column-side shifts beta of the line
+// (both zero before the first absorption) and g_r = z_r - z_{r-1}:
+//   rho_r   = exp((-g_r + alpha_r - alpha_{r-1}) / eps)      lower ratio
+//   delta_r = exp((alpha_r + beta_r) / eps)                  diagonal edge
+//   sigma_r = exp((-g_{r+1} + alpha_r - alpha_{r+1}) / eps)  upper ratio
+//   mu_r    = exp((-g_{r+1} + alpha_r + beta_{r+1}) / eps)   upper edge
+// -- the reference's exponent expressions (kernel1d.py:121-159, dyn form
+// _kernels.py:128-203), evaluated once per absorption epoch.
+//
+// Records per tile of SQT = 256 points (lane l holds points 8l .. 8l+7):
+//   F: (rho, delta) then (sigma, mu), double2 at [j][k][lane]   (8 KB)
+//   W: (wf, wb) double2 at [k][lane], the tile-map weights      (4 KB)
+//      wf_r = delta_r prod_{s > r} rho_s, wb_r = mu_r prod_{s < r} sigma_s
+//   S: (prod rho, prod sigma) of the tile
+// so a tile's maps for values v are P_last = S.x P_in + sum wf v and
+// Q_first = S.y Q_after + sum wb v_{+1} (k_sq_pre), resolved along the line
+// (k_sq_scan) and applied (k_sq_apply).
+#pragma once
+
+namespace fb {
+
+constexpr int SQT = 32 * EPT;          // points per tile
+constexpr int SQF = 2 * EPT * 32;      // double2 of F per tile
+constexpr int SQW = EPT * 32;          // double2 of W per tile
+
+struct SqArgs {
+  const double *Z;        // the line mesh (z[0..n))
+  const double *alpha;    // nullable: row-side shifts, line p at alpha + p * n
+  const double *beta;     // nullable: column-side shifts, same layout
+  double2 *F, *W, *S;     // records (shared: one line's worth)
+  Node *nodes;            // per (line, tile): maps / exclusive maps
+  const double *vin;      // input values, line p at vin + p * n
+  double *out_t;          // output, transposed: out_t[r * lines + p]
+  int n, lines, tl;       // points per line, lines, tiles per line
+  int shared;             // records shared by every line (no shifts)
+  double inv;             // 1 / eps
+};
+
+// Records of one tile (warp per (line, tile); shared records: line 0 only).
+__global__ void __launch_bounds__(NTHR) k_sq_build(SqArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * WPC + (threadIdx.x >> 5);
+  const int nl = a.shared ? 1 : a.lines;
+  if (w >= (long long)nl * a.tl) return;
+  const int p = (int)(w / a.tl), t = (int)(w % a.tl);
+  const double *al = a.alpha ? a.alpha + (size_t)p * a.n : nullptr;
+  const double *be = a.beta ? a.beta + (size_t)p * a.n : nullptr;
+  auto A = [&](int r) { return al ? al[r] : 0.0; };
+  auto B = [&](int r) { return be ? be[r] : 0.0; };
+  const int r0 = t * SQT + EPT * lane;
+  double rho[EPT], del[EPT], sig[EPT], mu[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int r = r0 + k;
+    rho[k] = 1.0; del[k] = 0.0; sig[k] = 1.0; mu[k] = 0.0;  // padding: identity steps
+    if (r < a.n) {
+      del[k] = exp(__dmul_rn(__dadd_rn(A(r), B(r)), a.inv));
+      if (r > 0)
+        rho[k] = exp(__dmul_rn(__dadd_rn(-(a.Z[r] - a.Z[r - 1]), __dsub_rn(A(r), A(r - 1))), a.inv));
+      if (r + 1 < a.n) {
+        const double g = a.Z[r + 1] - a.Z[r];
+        sig[k] = exp(__dmul_rn(__dadd_rn(-g, __dsub_rn(A(r), A(r + 1))), a.inv));
+        mu[k] = exp(__dmul_rn(__dadd_rn(-g, __dadd_rn(A(r), B(r + 1))), a.inv));
+      }
+    }
+  }
+  // in-lane suffix products of rho (after k) and prefix products of sigma (before k)
+  double sp[EPT], pp[EPT];
+  sp[EPT - 1] = 1.0;
+  for (int k = EPT - 2; k >= 0; --k) sp[k] = __dmul_rn(rho[k + 1], sp[k + 1]);
+  pp[0] = 1.0;
+  for (int k = 1; k < EPT; ++k) pp[k] = __dmul_rn(sig[k - 1], pp[k - 1]);
+  const double rt = __dmul_rn(rho[0], sp[0]), st = __dmul_rn(sig[EPT - 1], pp[EPT - 1]);
+  // across lanes: products of later lanes' rho, of earlier lanes' sigma
+  double sx = rt, px = st;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double o1 = __shfl_down_sync(0xffffffffu, sx, off);
+    const double o2 = __shfl_up_sync(0xffffffffu, px, off);
+    if (lane + off < 32) sx = __dmul_rn(sx, o1);
+    if (lane >= off) px = __dmul_rn(o2, px);
+  }
+  // inclusive -> exclusive
+  double sxe = __shfl_down_sync(0xffffffffu, sx, 1), pxe = __shfl_up_sync(0xffffffffu, px, 1);
+  if (lane == 31) sxe = 1.0;
+  if (lane == 0) pxe = 1.0;
+  const size_t tile = (size_t)p * a.tl + t;
+  double2 *F = a.F + tile * SQF, *W = a.W + tile * SQW;
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    F[k * 32 + lane] = make_double2(rho[k], del[k]);
+    F[(EPT + k) * 32 + lane] = make_double2(sig[k], mu[k]);
+    W[k * 32 + lane] = make_double2(__dmul_rn(del[k], __dmul_rn(sp[k], sxe)),
+                                    __dmul_rn(mu[k], __dmul_rn(pp[k], pxe)));
+  }
+  const double af = __shfl_sync(0xffffffffu, sx, 0), ab = __shfl_sync(0xffffffffu, px, 31);
+  if (lane == 0) a.S[tile] = make_double2(af, ab);
+}
+
+// This lane's v_r for r = r0 .. r0 + EPT (EPT + 1 values, zero past the line).
+__device__ __forceinline__ void sq_load_v(const double *v, int r0, int n, double (&x)[EPT + 1]) {
+#pragma unroll
+  for (int k = 0; k <= EPT; ++k) x[k] = r0 + k < n ? __ldg(v + r0 + k) : 0.0;
+}
+
+// The tiles' maps for the input values: tf = (prod rho, 0, sum wf v, 1, 0),
+// tb = (prod sigma, 0, sum wb v_{+1}, 1, 0) in the Tf encoding
+// (p' = A p + C; acc unused), written as the tile's node.
+__global__ void __launch_bounds__(NTHR) k_sq_pre(SqArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * WPC + (threadIdx.x >> 5);
+  if (w >= (long long)a.lines * a.tl) return;
+  const int p = (int)(w / a.tl), t = (int)(w % a.tl);
+  const size_t rec = a.shared ? (size_t)t : (size_t)w;
+  const double2 *W = a.W + rec * SQW;
+  double x[EPT + 1];
+  sq_load_v(a.vin + (size_t)p * a.n, t * SQT + EPT * lane, a.n, x);
+  double cf = 0.0, cb = 0.0;
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const double2 wk = __ldg(W + k * 32 + lane);
+    cf = __fma_rn(wk.x, x[k], cf);
+    cb = __fma_rn(wk.y, x[k + 1], cb);
+  }
+  cf = warp_sum(cf);
+  cb = warp_sum(cb);
+  if (lane == 0) {
+    const double2 s = __ldg(a.S + rec);
+    Node *nd = a.nodes + w;
+    nd->tf = Tf{s.x, 0.0, cf, 1.0, 0.0};
+    nd->tb = Tf{s.y, 0.0, cb, 1.0, 0.0};
+  }
+}
+
+// Exclusive maps of every tile along its line (warp per line, chunks of 32
+// tiles carried across chunks; guarded compositions as across 1D tiles).
+__global__ void __launch_bounds__(NTHR) k_sq_scan(SqArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * WPC + (threadIdx.x >> 5);
+  if (p >= a.lines) return;
+  Node *lv = a.nodes + (size_t)p * a.tl;
+  const int n = a.tl, nch = (n + 31) / 32;
+  Tf cf = tf_id(), cb = tf_id();
+  for (int c = 0; c < nch; ++c) {
+    const int lt = 32 * c + lane;
+    const bool have = lt < n;
+    const Tf f = have ? ldcg_tf(&lv[lt].tf) : tf_id();
+    const Tf b = have && nch == 1 ? ldcg_tf(&lv[lt].tb) : tf_id();
+    Tf xf, xb, totf, totb;
+    warp_scan2<true>(f, b, xf, xb, totf, totb);
+    if (have) {
+      lv[lt].xf = tf_cat_g(cf, xf);
+      if (nch == 1) lv[lt].xb = xb;
+    }
+    cf = tf_cat_g(cf, totf);
+  }
+  for (int c = nch - 1; nch > 1 && c >= 0; --c) {
+    const int lt = 32 * c + lane;
+    const bool have = lt < n;
+    const Tf b = have ? ldcg_tf(&lv[lt].tb) : tf_id();
+    Tf xf, xb, totf, totb;
+    warp_scan2<true>(tf_id(), b, xf, xb, totf, totb);
+    if (have) lv[lt].xb = tf_cat_g(cb, xb);
+    cb = tf_cat_g(cb, totb);
+  }
+}
+
+// The sweep: CTA = tile t of WPC consecutive lines; lane l walks points
+// 8l .. 8l+7 of its warp's tile.  Lane maps of both recurrences, two warp
+// scans (the tile's incoming P / Q folded into the end lanes), the final
+// recurrences in the reference's operation order ((r * p) + acc, p + q),
+// then the CTA writes the rows transposed (four lines per 32-byte sector).
+__global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
+  __shared__ double so[WPC][SQT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x % a.tl, p0 = (blockIdx.x / a.tl) * WPC, p = p0 + warp;
+  const int r0 = t * SQT + EPT * lane;
+  if (p < a.lines) {
+    const size_t tile = (size_t)p * a.tl + t;
+    const size_t rec = a.shared ? (size_t)t : tile;
+    const double2 *F = a.F + rec * SQF;
+    double2 f0[EPT], f1[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      f0[k] = __ldcs(F + k * 32 + lane);
+      f1[k] = __ldcs(F + (EPT + k) * 32 + lane);
+    }
+    double x[EPT + 1];
+    sq_load_v(a.vin + (size_t)p * a.n, r0, a.n, x);
+    double pin = 0.0, qin = 0.0;  // the tile's incoming P (lane 0) / Q (lane 31)
+    if (lane == 0) pin = __ldcg(&a.nodes[tile].xf.C);
+    if (lane == 31) qin = __ldcg(&a.nodes[tile].xb.C);
+    // lane maps: forward P_end = af P_in + cf, backward Q_first = ab Q_after + cb
+    double af = 1.0, cf = 0.0, ab = 1.0, cb = 0.0;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      f0[k].y = __dmul_rn(f0[k].y, x[k]);      // delta v
+      f1[k].y = __dmul_rn(f1[k].y, x[k + 1]);  // mu v_{+1}
+      af = __dmul_rn(f0[k].x, af);
+      cf = __dadd_rn(__dmul_rn(f0[k].x, cf), f0[k].y);
+    }
+#pragma unroll
+    for (int k = EPT - 1; k >= 0; --k) {
+      ab = __dmul_rn(f1[k].x, ab);
+      cb = __dadd_rn(__dmul_rn(f1[k].x, cb), f1[k].y);
+    }
+    // fold the tile's inputs into the end lanes, then inclusive scans
+    if (lane == 0) { cf = __fma_rn(af, pin, cf); af = 0.0; }
+    if (lane == 31) { cb = __fma_rn(ab, qin, cb); ab = 0.0; }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double oa = __shfl_up_sync(0xffffffffu, af, off);
+      const double oc = __shfl_up_sync(0xffffffffu, cf, off);
+      const double ob = __shfl_down_sync(0xffffffffu, ab, off);
+      const double od = __shfl_down_sync(0xffffffffu, cb, off);
+      if (lane >= off) { cf = __fma_rn(af, oc, cf); af = __dmul_rn(af, oa); }
+      if (lane + off < 32) { cb = __fma_rn(ab, od, cb); ab = __dmul_rn(ab, ob); }
+    }
+    double pp = __shfl_up_sync(0xffffffffu, cf, 1), qq = __shfl_down_sync(0xffffffffu, cb, 1);
+    if (lane == 0) pp = pin;
+    if (lane == 31) qq = qin;
+    // final recurrences (_kernels.py:65-67 / :80-87 order)
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      pp = __dadd_rn(__dmul_rn(f0[k].x, pp), f0[k].y);
+      f0[k].y = pp;
+    }
+#pragma unroll
+    for (int k = EPT - 1; k >= 0; --k) {
+      qq = __dadd_rn(__dmul_rn(f1[k].x, qq), f1[k].y);
+      so[warp][EPT * lane + k] = __dadd_rn(f0[k].y, qq);
+    }
+  }
+  __syncthreads();
+  const int cnt = min(SQT, a.n - t * SQT);
+  for (int k = threadIdx.x; k < cnt * WPC; k += NTHR) {
+    const int i = k / WPC, w = k % WPC;
+    if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = so[w][i];
+  }
+}
+
+}  // namespace fb

@@ -79,6 +79,26 @@ def test_config3_full_vs_reference_pins():
     assert q["hist"] < 1 and q["phi"] < TOL and q["psi"] < TOL and q["cost"] < TOL, q
 
 
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "config4_full_pins.npz")),
+                    reason="config-4 pins not generated")
+def test_config4_full_vs_reference_pins():
+    """Full-size config 4 (8192^2, 100 it, 3 absorptions) against the
+    reference's own run (tests/golden/make_golden.py config4_full)."""
+    g = load_golden("config4_full_pins.npz")
+    x1, y1, x2, y2, U, V, eps = W.config4()
+    sol = fb.sinkhorn_2d(_grid(x1, y1), _grid(x2, y2), fb.Measure2D(U), fb.Measure2D(V),
+                         fb.SolverConfig(epsilon=eps, itr_max=100, tol=0.0, stabilize=True))
+    st = int(g["stride"])
+    from test_parity_gpu import hist_ok
+    q = dict(hist=hist_ok([h[1] for h in sol.marginal_error_history], g["hist_err"]),
+             phi=rel_inf(sol.phi[::st], g["phi_s"]), psi=rel_inf(sol.psi[::st], g["psi_s"]),
+             a=rel_inf(sol.a[::st], g["a_s"]), b=rel_inf(sol.b[::st], g["b_s"]),
+             cost=abs(sol.cost - float(g["cost"])) / abs(float(g["cost"])))
+    print("config4 full parity", q)
+    assert list(sol.absorb_iterations) == [int(t) for t in g["absorb_its"]]
+    assert q["hist"] < 1 and q["phi"] < TOL and q["psi"] < TOL and q["cost"] < TOL, q
+
+
 def _sharded_case(n, m1, m2, eps, itr, seed, zero_rows=False, thr=200.0):
     rng = np.random.default_rng(seed)
     x = W.gap_mesh(rng, n, 0.1, 1.9)
