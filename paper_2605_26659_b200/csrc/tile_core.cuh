@@ -224,6 +224,23 @@ __device__ __forceinline__ double warp_sum4(double q0, double q1, double q2, dou
 // the children's partials in a fixed order, and arrives one level up.  The
 // warp completing the problem node runs the per-problem epilogue (control
 // logic).  A consumer's carry is the composition of <= 3 exclusive maps.
+// Timing experiment (FB_DBG_RES builds only): globaltimer stamps of the
+// resolve chain for one iteration, max (or min, stored complemented) over
+// the warps that reach the point.
+#ifdef FB_DBG_RES
+__device__ unsigned long long g_phase[16];
+__device__ __forceinline__ void res_stamp(int slot, bool is_min) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMax(&g_phase[slot], is_min ? ~t : t);
+}
+#define RES_STAMP(cond, slot, mn) \
+  do {                             \
+    if (cond) res_stamp(slot, mn); \
+  } while (0)
+#else
+#define RES_STAMP(cond, slot, mn)
+#endif
 struct Node {
   Tf tf, tb;   // totals over the subtree (forward / backward)
   Tf xf, xb;   // exclusive maps within the parent
@@ -281,6 +298,7 @@ __device__ __forceinline__ bool tree_arrive_from(const Resolve &R, const TreeGeo
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) return false;
+    RES_STAMP(lane == 0 && L < 3 && g_phase[10] != 0 && g_phase[14] == 0, 11 + L, false);
 #ifndef FB_ACQREL
     __threadfence();
 #endif
