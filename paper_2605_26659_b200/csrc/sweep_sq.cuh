@@ -32,6 +32,38 @@
 
 namespace fb {
 
+// Partials of the 2D scaling update (k_epi2d, fused square sweeps).
+struct EpiPart {
+  double err, vmax, vmin;
+  long long fail;  // min over failing flat indices of (idx << 2) | status; LLONG_MAX if none
+};
+// The CTA's partial in a fixed order: warp trees, then thread 0 folds the warps.
+__device__ __forceinline__ void epi_block_part(double err, double vmax, double vmin,
+                                               long long fail, EpiPart *out) {
+  __shared__ EpiPart sp[32];
+  err = warp_sum(err);
+  vmax = warp_max(vmax);
+  vmin = warp_min(vmin);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const long long o = __shfl_xor_sync(0xffffffffu, fail, off);
+    fail = o < fail ? o : fail;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sp[warp] = EpiPart{err, vmax, vmin, fail};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    EpiPart r{0.0, 0.0, INFINITY, LLONG_MAX};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      r.err += sp[w].err;
+      r.vmax = fmax(r.vmax, sp[w].vmax);
+      r.vmin = fmin(r.vmin, sp[w].vmin);
+      r.fail = sp[w].fail < r.fail ? sp[w].fail : r.fail;
+    }
+    *out = r;
+  }
+}
+
 constexpr int SQT = 32 * EPT;          // points per tile
 constexpr int SQF = 2 * EPT * 32;      // double2 of F per tile
 constexpr int SQW = EPT * 32;          // double2 of W per tile
@@ -47,6 +79,13 @@ struct SqArgs {
   int n, lines, tl;       // points per line, lines, tiles per line
   int shared;             // records shared by every line (no shifts)
   double inv;             // 1 / eps
+  // fused scaling update (nullable ew: plain sweep): SC <- W / out over the
+  // flat grid out_t addresses, marginal error (eerr), extremes, failures;
+  // per-CTA partials into epart (k_epi_fold reduces them in a fixed order)
+  const double *ew;
+  double *esc;
+  EpiPart *epart;
+  int eerr;
 };
 
 // Records of one tile (warp per (line, tile); shared records: line 0 only).
@@ -246,10 +285,38 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
   }
   __syncthreads();
   const int cnt = min(SQT, a.n - t * SQT);
+  if (!a.ew) {
+    for (int k = threadIdx.x; k < cnt * WPC; k += NTHR) {
+      const int i = k / WPC, w = k % WPC;
+      if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = so[w][i];
+    }
+    return;
+  }
+  // the grid's scaling update on the same addresses (k_epi2d's rules,
+  // _kernels.py:376-397 / :408-427): no T round trip through HBM
+  double err = 0.0, vmax = 0.0, vmin = INFINITY;
+  long long fail = LLONG_MAX;
   for (int k = threadIdx.x; k < cnt * WPC; k += NTHR) {
     const int i = k / WPC, w = k % WPC;
-    if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = so[w][i];
+    if (p0 + w >= a.lines) continue;
+    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+    const double wv = __ldcs(a.ew + idx), tt = so[w][i];
+    if (a.eerr) err = __dadd_rn(err, fabs(__dsub_rn(__dmul_rn(a.esc[idx], tt), wv)));
+    double nv;
+    if (tt == 0.0) {
+      if (wv > 0.0) fail = min(fail, (idx << 2) | ST_ZD);
+      nv = 0.0;
+    } else {
+      nv = __ddiv_rn(wv, tt);
+      if (!isfinite(nv)) fail = min(fail, (idx << 2) | ST_NF);
+      else if (wv > 0.0) {
+        vmax = fmax(vmax, nv);
+        vmin = fmin(vmin, nv);
+      }
+    }
+    a.esc[idx] = nv;
   }
+  epi_block_part(err, vmax, vmin, fail, a.epart + blockIdx.x);
 }
 
 }  // namespace fb
