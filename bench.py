@@ -163,6 +163,13 @@ def run_2d(args, cfg, wl, world=1, rank=0):
     loop = statistics.median(loops)
     if rank != 0:
         return
+    # roofline of the whole iteration: 88 B/pt before the first
+    # absorption, 120 B/pt after (the two-sweep algorithm with a materialised
+    # intermediate), weighted by the iterations spent in either state
+    a0 = sol.absorb_iterations[0] if len(sol.absorb_iterations) else sol.iterations_run
+    abytes = pts * (88.0 * a0 + 120.0 * (sol.iterations_run - a0))
+    peak, psrc = peaks()
+    achieved = abytes / loop / 1e9
     line = {
         "metric": METRIC, "value": pts * wl["itr"] / loop, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * loop,
@@ -172,7 +179,15 @@ def run_2d(args, cfg, wl, world=1, rank=0):
         "config": {"workload": "config%d: 2D %dx%d eps=%g %d it (stabilize=True)" % (
             cfg, x1.size, y1.size, wl["eps"][0], wl["itr"]), "itr_max": wl["itr"],
             "parallelism": "row shards x%d (carry exchange)" % world if world > 1 else "1 GPU",
-            "timing": "loop window (max over ranks); host-driven loop, one sync per iteration"},
+            "timing": "loop window (max over ranks); " + (
+                "host-driven loop, one sync per iteration" if world > 1 else
+                "device-looped CUDA graph, host sync only at absorptions")},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": psrc,
+                     "kernel": "whole iteration: 4 line sweeps (k_sq_pre/k_sq_scan/k_sq_apply) "
+                               "+ fused scaling updates",
+                     "algorithmic_bytes_per_solve": abytes,
+                     "bytes_rule": "88 B/pt unabsorbed, 120 B/pt absorbed (SURVEY 8d)"},
         "e2e": {"value": pts * wl["itr"] / statistics.median(walls), "unit": UNIT,
                 "h2d_bytes_per_step": 8 * (2 * pts + 2 * x1.size + 2 * y1.size),
                 "d2h_bytes_per_step": 8 * 4 * pts},
