@@ -87,13 +87,32 @@ __device__ __forceinline__ Tf tf_shfl_down(const Tf &f, int d) {
             __shfl_down_sync(0xffffffffu, f.E, d)};
 }
 
+__device__ __forceinline__ bool tf_finite(const Tf &f) {
+  return isfinite(f.A) && isfinite(f.B) && isfinite(f.C) && isfinite(f.D) && isfinite(f.E);
+}
+
+// g o f, guarded only if an input is not finite (the guard matters for 0 * inf only).
+__device__ __forceinline__ Tf tf_cat_f(const Tf &f, const Tf &g) {
+  if (tf_finite(f) && tf_finite(g)) return tf_cat(f, g);
+  return tf_cat_g(f, g);
+}
+
 // Warp scans of per-lane maps.  Exclusive results: xf = maps of lanes < lane
 // (lane 0 first), xb = maps of lanes > lane (lane 31 first); inclusive totals
-// returned in all lanes.  G selects the guarded composition.
+// returned in all lanes.  G selects the guarded composition; the guarded
+// scan first tries the plain one, which agrees with it (up to fma
+// contraction) whenever nothing is infinite: the guard only matters for
+// 0 * inf, so it is kept for warps whose inputs or results are not finite.
 template <bool G>
 __device__ __forceinline__ void warp_scan2(const Tf &f, const Tf &b, Tf &xf, Tf &xb, Tf &totf,
                                            Tf &totb) {
   const int lane = threadIdx.x & 31;
+  if (G && __all_sync(0xffffffffu, tf_finite(f) && tf_finite(b))) {
+    warp_scan2<false>(f, b, xf, xb, totf, totb);
+    if (__all_sync(0xffffffffu, tf_finite(xf) && tf_finite(xb) && tf_finite(totf) &&
+                                    tf_finite(totb)))
+      return;
+  }
   Tf incf = f, incb = b;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {

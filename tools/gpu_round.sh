@@ -15,5 +15,5 @@ python tools/launch_summary.py gpurun_out/launches.csv | head -12
 export ITERS=3
 timeout 600 python tools/ncu_target.py > gpurun_out/plain.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 2 -c 2 -o gpurun_out/prof_kstep python tools/ncu_target.py > gpurun_out/ncu2.log 2>&1; echo "ncu rc=$?"
-CFG=3 ITERS=6 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launch3.csv python tools/ncu_2d_target.py > /dev/null 2>&1; echo rc3=$?
-CFG=4 ITERS=10 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launch4.csv python tools/ncu_2d_target.py > /dev/null 2>&1; echo rc4=$?
+CFG=3 ITERS=6 FB_GRAPH2D=0 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launch3.csv python tools/ncu_2d_target.py > /dev/null 2>&1; echo rc3=$?
+CFG=4 ITERS=10 FB_GRAPH2D=0 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launch4.csv python tools/ncu_2d_target.py > /dev/null 2>&1; echo rc4=$?
