@@ -17,7 +17,10 @@
 
 namespace fb {
 
-constexpr int EPT = 8;                  // merged elements per lane
+#ifndef FB_EPT
+#define FB_EPT 8
+#endif
+constexpr int EPT = FB_EPT;             // merged elements per lane
 constexpr int NSLOT = 32 * EPT;         // slots per warp tile
 constexpr int TILE = NSLOT - 1;         // merged elements per tile (+1 tie slack)
 constexpr int RPT = EPT;                // rows per lane in the epilogue (upper bound)

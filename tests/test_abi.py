@@ -96,6 +96,42 @@ def test_tile_partition_properties(n, m, ties):
             assert got == [int(b) for b in bits]
 
 
+@pytest.mark.parametrize("ties", [False, True])
+def test_tile_partition_parallel_segments(ties):
+    """Problems of >= 2^20 merged elements are tiled in 16 host-threaded segments:
+    the partition stays contiguous, within the tile size, never splits a tie,
+    and its merged-order masks are right at the segment joins."""
+    from paper_2605_26659_b200 import _lib
+    rng = np.random.default_rng(7)
+    n = 600_000
+    x = np.sort(rng.uniform(0, 1, n))
+    y = x.copy() if ties else np.sort(rng.uniform(0, 1, n + 123))
+    tiles, masks = _lib.tile_partition(x, y)
+    x0, x1, y0, y1 = (tiles[:, k].astype(np.int64) for k in range(4))
+    assert x0[0] == 0 and y0[0] == 0 and x1[-1] == x.size and y1[-1] == y.size
+    assert np.all(x0[1:] == x1[:-1]) and np.all(y0[1:] == y1[:-1])
+    sz = (x1 - x0) + (y1 - y0)
+    assert sz.min() > 0 and sz.max() <= 256
+    # no tie split: every element of tile t lies strictly above the last x / y before it
+    lo = np.minimum(np.where(x1 > x0, x[np.minimum(x0, x.size - 1)], np.inf),
+                    np.where(y1 > y0, y[np.minimum(y0, y.size - 1)], np.inf))
+    prev = np.maximum(np.where(x0 > 0, x[np.maximum(x0 - 1, 0)], -np.inf),
+                      np.where(y0 > 0, y[np.maximum(y0 - 1, 0)], -np.inf))
+    assert np.all(lo > prev)
+    # masks of the tiles around the segment joins (and a few others)
+    N = x.size + y.size
+    picks = {0, len(tiles) - 1}
+    for s in range(1, 16):
+        t = int(np.searchsorted(x0 + y0, N * s // 16, side="right")) - 1
+        picks.update({max(t - 1, 0), t, min(t + 1, len(tiles) - 1)})
+    for t in sorted(picks):
+        for half in (0, 1):
+            bits = _merge_ref(x[x0[t]:x1[t]], y[y0[t]:y1[t]], half)
+            word = masks[t, half * 8:(half + 1) * 8]
+            got = [(int(word[k // 32]) >> (k % 32)) & 1 for k in range(len(bits))]
+            assert got == [int(b) for b in bits]
+
+
 def test_fexp_host_arithmetic():
     """csrc/fexp.cuh's q_div is the IEEE quotient and fexp is within 1 ulp of libm exp."""
     exe = "/tmp/finom_fexp_check"
