@@ -149,10 +149,26 @@ __global__ void __launch_bounds__(NTHR) k_sq_build(SqArgs a) {
   if (lane == 0) a.S[tile] = make_double2(af, ab);
 }
 
-// This lane's v_r for r = r0 .. r0 + EPT (EPT + 1 values, zero past the line).
-__device__ __forceinline__ void sq_load_v(const double *v, int r0, int n, double (&x)[EPT + 1]) {
+// This lane's v_r for r = t0 + EPT lane .. + EPT (EPT + 1 values, zero past
+// the line): the warp's SQT + 1 values are loaded coalesced into xs (one pad
+// double per EPT, so the lanes' EPT-strided reads hit distinct banks), then
+// each lane reads its run.  (A lane reading its run straight from global
+// memory touches 32 sectors per instruction.)
+constexpr int SQX = SQT + SQT / EPT + 2;  // staging doubles per warp
+__device__ __forceinline__ int sq_pad(int i) { return i + i / EPT; }
+__device__ __forceinline__ void sq_load_v(const double *v, int t0, int n, double *xs,
+                                          double (&x)[EPT + 1]) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int k = 0; k <= EPT; ++k) x[k] = r0 + k < n ? __ldg(v + r0 + k) : 0.0;
+  for (int k = 0; k < EPT; ++k) {
+    const int i = lane + 32 * k;
+    xs[sq_pad(i)] = t0 + i < n ? __ldg(v + t0 + i) : 0.0;
+  }
+  if (lane == 0) xs[sq_pad(SQT)] = t0 + SQT < n ? __ldg(v + t0 + SQT) : 0.0;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k <= EPT; ++k) x[k] = xs[sq_pad(EPT * lane + k)];
+  __syncwarp();
 }
 
 // The tiles' maps for the input values: tf = (prod rho, 0, sum wf v, 1, 0),
@@ -165,8 +181,9 @@ __global__ void __launch_bounds__(NTHR) k_sq_pre(SqArgs a) {
   const int p = (int)(w / a.tl), t = (int)(w % a.tl);
   const size_t rec = a.shared ? (size_t)t : (size_t)w;
   const double2 *W = a.W + rec * SQW;
+  __shared__ double xs[WPC][SQX];
   double x[EPT + 1];
-  sq_load_v(a.vin + (size_t)p * a.n, t * SQT + EPT * lane, a.n, x);
+  sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, xs[threadIdx.x >> 5], x);
   double cf = 0.0, cb = 0.0;
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
@@ -223,10 +240,9 @@ __global__ void __launch_bounds__(NTHR) k_sq_scan(SqArgs a) {
 // recurrences in the reference's operation order ((r * p) + acc, p + q),
 // then the CTA writes the rows transposed (four lines per 32-byte sector).
 __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
-  __shared__ double so[WPC][SQT];
+  __shared__ double so[WPC][SQX];  // input staging, then the tile's outputs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x % a.tl, p0 = (blockIdx.x / a.tl) * WPC, p = p0 + warp;
-  const int r0 = t * SQT + EPT * lane;
   if (p < a.lines) {
     const size_t tile = (size_t)p * a.tl + t;
     const size_t rec = a.shared ? (size_t)t : tile;
@@ -238,7 +254,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
       f1[k] = __ldcs(F + (EPT + k) * 32 + lane);
     }
     double x[EPT + 1];
-    sq_load_v(a.vin + (size_t)p * a.n, r0, a.n, x);
+    sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, so[warp], x);
     double pin = 0.0, qin = 0.0;  // the tile's incoming P (lane 0) / Q (lane 31)
     if (lane == 0) pin = __ldcg(&a.nodes[tile].xf.C);
     if (lane == 31) qin = __ldcg(&a.nodes[tile].xb.C);
