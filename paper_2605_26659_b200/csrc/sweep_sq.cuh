@@ -312,12 +312,24 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
   // _kernels.py:376-397 / :408-427): no T round trip through HBM
   double err = 0.0, vmax = 0.0, vmin = INFINITY;
   long long fail = LLONG_MAX;
-  for (int k = threadIdx.x; k < cnt * WPC; k += NTHR) {
-    const int i = k / WPC, w = k % WPC;
-    if (p0 + w >= a.lines) continue;
+  // every load of the thread's elements is issued before the first use
+  constexpr int EPER = SQT * WPC / NTHR;
+  double wq[EPER], sq[EPER];
+#pragma unroll
+  for (int q = 0; q < EPER; ++q) {
+    const int k = threadIdx.x + q * NTHR, i = k / WPC, w = k % WPC;
+    const bool live = k < cnt * WPC && p0 + w < a.lines;
     const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
-    const double wv = __ldcs(a.ew + idx), tt = so[w][i];
-    if (a.eerr) err = __dadd_rn(err, fabs(__dsub_rn(__dmul_rn(a.esc[idx], tt), wv)));
+    wq[q] = live ? __ldcs(a.ew + idx) : 0.0;
+    sq[q] = live && a.eerr ? __ldcs(a.esc + idx) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < EPER; ++q) {
+    const int k = threadIdx.x + q * NTHR, i = k / WPC, w = k % WPC;
+    if (k >= cnt * WPC || p0 + w >= a.lines) continue;
+    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+    const double wv = wq[q], tt = so[w][i];
+    if (a.eerr) err = __dadd_rn(err, fabs(__dsub_rn(__dmul_rn(sq[q], tt), wv)));
     double nv;
     if (tt == 0.0) {
       if (wv > 0.0) fail = min(fail, (idx << 2) | ST_ZD);
