@@ -73,6 +73,11 @@ struct SqArgs {
   const double *alpha;    // nullable: row-side shifts, line p at alpha + p * n
   const double *beta;     // nullable: column-side shifts, same layout
   double2 *F, *W, *S;     // records (shared: one line's worth)
+  // split records (column-side shifts only): F, S shared (the ratios do not
+  // depend on beta), W shared raw factors (prod rho, prod sigma parts), and
+  // per line only D = (delta, mu), double2 at [tile][k][lane]
+  double2 *D;
+  int wraw;               // k_sq_build: write W as the raw factors (split mode)
   Node *nodes;            // per (line, tile): maps / exclusive maps
   const double *vin;      // input values, line p at vin + p * n
   double *out_t;          // output, transposed: out_t[r * lines + p]
@@ -142,11 +147,35 @@ __global__ void __launch_bounds__(NTHR) k_sq_build(SqArgs a) {
   for (int k = 0; k < EPT; ++k) {
     F[k * 32 + lane] = make_double2(rho[k], del[k]);
     F[(EPT + k) * 32 + lane] = make_double2(sig[k], mu[k]);
-    W[k * 32 + lane] = make_double2(__dmul_rn(del[k], __dmul_rn(sp[k], sxe)),
-                                    __dmul_rn(mu[k], __dmul_rn(pp[k], pxe)));
+    W[k * 32 + lane] = a.wraw ? make_double2(__dmul_rn(sp[k], sxe), __dmul_rn(pp[k], pxe))
+                              : make_double2(__dmul_rn(del[k], __dmul_rn(sp[k], sxe)),
+                                             __dmul_rn(mu[k], __dmul_rn(pp[k], pxe)));
   }
   const double af = __shfl_sync(0xffffffffu, sx, 0), ab = __shfl_sync(0xffffffffu, px, 31);
   if (lane == 0) a.S[tile] = make_double2(af, ab);
+}
+
+// Per-line (delta, mu) of the split records: k_sq_build's expressions with
+// alpha = 0 (warp per (line, tile)).
+__global__ void __launch_bounds__(NTHR) k_sq_build_d(SqArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * WPC + (threadIdx.x >> 5);
+  if (w >= (long long)a.lines * a.tl) return;
+  const int p = (int)(w / a.tl), t = (int)(w % a.tl);
+  const double *be = a.beta + (size_t)p * a.n;
+  const int r0 = t * SQT + EPT * lane;
+  double2 *D = a.D + (size_t)w * SQW;
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int r = r0 + k;
+    double del = 0.0, mu = 0.0;
+    if (r < a.n) {
+      del = exp(__dmul_rn(__dadd_rn(0.0, be[r]), a.inv));
+      if (r + 1 < a.n)
+        mu = exp(__dmul_rn(__dadd_rn(-(a.Z[r + 1] - a.Z[r]), __dadd_rn(0.0, be[r + 1])), a.inv));
+    }
+    D[k * 32 + lane] = make_double2(del, mu);
+  }
 }
 
 // This lane's v_r for r = t0 + EPT lane .. + EPT (EPT + 1 values, zero past
@@ -179,15 +208,20 @@ __global__ void __launch_bounds__(NTHR) k_sq_pre(SqArgs a) {
   const long long w = (long long)blockIdx.x * WPC + (threadIdx.x >> 5);
   if (w >= (long long)a.lines * a.tl) return;
   const int p = (int)(w / a.tl), t = (int)(w % a.tl);
-  const size_t rec = a.shared ? (size_t)t : (size_t)w;
+  const size_t rec = a.shared || a.D ? (size_t)t : (size_t)w;
   const double2 *W = a.W + rec * SQW;
+  const double2 *D = a.D ? a.D + (size_t)w * SQW : nullptr;
   __shared__ double xs[WPC][SQX];
   double x[EPT + 1];
   sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, xs[threadIdx.x >> 5], x);
   double cf = 0.0, cb = 0.0;
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
-    const double2 wk = __ldg(W + k * 32 + lane);
+    double2 wk = __ldg(W + k * 32 + lane);
+    if (D) {  // split records: the same products as k_sq_build's W
+      const double2 dk = __ldcs(D + k * 32 + lane);
+      wk = make_double2(__dmul_rn(dk.x, wk.x), __dmul_rn(dk.y, wk.y));
+    }
     cf = __fma_rn(wk.x, x[k], cf);
     cb = __fma_rn(wk.y, x[k + 1], cb);
   }
@@ -245,13 +279,23 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
   const int t = blockIdx.x % a.tl, p0 = (blockIdx.x / a.tl) * WPC, p = p0 + warp;
   if (p < a.lines) {
     const size_t tile = (size_t)p * a.tl + t;
-    const size_t rec = a.shared ? (size_t)t : tile;
+    const size_t rec = a.shared || a.D ? (size_t)t : tile;
     const double2 *F = a.F + rec * SQF;
     double2 f0[EPT], f1[EPT];
+    if (a.D) {  // split records: shared ratios, the line's (delta, mu)
+      const double2 *D = a.D + tile * SQW;
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      f0[k] = __ldcs(F + k * 32 + lane);
-      f1[k] = __ldcs(F + (EPT + k) * 32 + lane);
+      for (int k = 0; k < EPT; ++k) {
+        const double2 dk = __ldcs(D + k * 32 + lane);
+        f0[k] = make_double2(__ldg(&F[k * 32 + lane].x), dk.x);
+        f1[k] = make_double2(__ldg(&F[(EPT + k) * 32 + lane].x), dk.y);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        f0[k] = __ldcs(F + k * 32 + lane);
+        f1[k] = __ldcs(F + (EPT + k) * 32 + lane);
+      }
     }
     double x[EPT + 1];
     sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, so[warp], x);
