@@ -7,7 +7,7 @@ public names mirror ``finom.solver``, ``finom.kernel1d`` and
 include/finom_b200.h.
 """
 
-from . import errors, kernel1d, kernel2d, mesh, solver  # noqa: F401
+from . import dense, errors, kernel1d, kernel2d, mesh, solver  # noqa: F401
 from .errors import *  # noqa: F401,F403
 from .mesh import Grid2D, Measure, Measure2D, Mesh1D, Problem  # noqa: F401
 from .solver import (  # noqa: F401
