@@ -175,3 +175,26 @@ def test_row_sharded_2d_nccl_world1():
     for key in ("phi", "psi", "a", "b"):
         assert rel_inf(getattr(a, key), getattr(b, key)) < 1e-11, key
     assert abs(a.cost - b.cost) <= 1e-11 * abs(b.cost)
+
+
+@pytest.mark.parametrize("env", [{"FB_GRAPH2D": "0"}, {"FB_SQ_SPLIT": "0"}, {"FB_SQ": "0"}])
+def test_2d_loop_variants_agree(monkeypatch, env):
+    """The device-looped graph vs the host-stepped loop (bitwise: same kernels),
+    split vs full square-sweep records and square vs general sweeps (1e-12):
+    absorbed config-3-style grid with a zero-mass stretch and a tol stop."""
+    x1, y1, x2, y2, U, V, eps = W.config3(n=96)
+    U = U.copy()
+    U[10:30, 40:50] = 0.0
+    U /= U.sum()
+    cfg = fb.SolverConfig(epsilon=eps, itr_max=60, tol=1e-7, stabilize=True, absorb_threshold=6.0)
+    args = (_grid(x1, y1), _grid(x2, y2), fb.Measure2D(U), fb.Measure2D(V), cfg)
+    base = fb.sinkhorn_2d(*args)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    alt = fb.sinkhorn_2d(*args)
+    assert base.iterations_run == alt.iterations_run and base.converged == alt.converged
+    assert list(base.absorb_iterations) == list(alt.absorb_iterations)
+    assert len(base.absorb_iterations) >= 1
+    tol = 0.0 if "FB_GRAPH2D" in env else 1e-12
+    assert rel_inf(alt.phi, base.phi) <= tol and rel_inf(alt.psi, base.psi) <= tol
+    assert abs(alt.cost - base.cost) <= max(tol, 1e-15) * abs(base.cost)

@@ -10,8 +10,8 @@ for n in (4096, 16384, 32768):
     x, y, u, v, eps = W.config1(n=n)
     X, Y, U, V = fb.Mesh1D(x), fb.Mesh1D(y), fb.Measure(u), fb.Measure(v)
     its = 100
-    cfg = fb.SolverConfig(epsilon=eps, itr_max=its, tol=0.0, stabilize=False)
-    D.dense_sinkhorn(fb.Problem(X, Y, U, V), fb.SolverConfig(epsilon=eps, itr_max=3, tol=0.0))
+    cfg = fb.SolverConfig(epsilon=eps, itr_max=its, tol=0.0, stabilize=False, plan_cap=10**10)
+    D.dense_sinkhorn(fb.Problem(X, Y, U, V), fb.SolverConfig(epsilon=eps, itr_max=3, tol=0.0, plan_cap=10**10))
     dn = D.dense_sinkhorn(fb.Problem(X, Y, U, V), cfg)
     bs = fb.BatchSolver1D([x], [y], [u], [v], [eps])
     bs.solve(its, 0.0, False, 200.0); torch.cuda.synchronize()

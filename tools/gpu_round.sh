@@ -17,3 +17,5 @@ timeout 600 python tools/ncu_target.py > gpurun_out/plain.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 2 -c 2 -o gpurun_out/prof_kstep python tools/ncu_target.py > gpurun_out/ncu2.log 2>&1; echo "ncu rc=$?"
 CFG=3 ITERS=6 FB_GRAPH2D=0 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launch3.csv python tools/ncu_2d_target.py > /dev/null 2>&1; echo rc3=$?
 CFG=4 ITERS=10 FB_GRAPH2D=0 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launch4.csv python tools/ncu_2d_target.py > /dev/null 2>&1; echo rc4=$?
+timeout 600 python tools/dense_vs_fast.py > gpurun_out/dense_vs_fast.txt 2>&1; cat gpurun_out/dense_vs_fast.txt | tail -4
+FB_VERBOSE=1 timeout 300 python tools/e2e_probe.py > gpurun_out/e2e_probe.txt 2>&1; tail -4 gpurun_out/e2e_probe.txt
