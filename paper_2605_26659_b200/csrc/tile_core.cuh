@@ -148,60 +148,13 @@ __device__ __forceinline__ double warp_min(double v) {
   return v;
 }
 
-// Lane-incoming states of one direction of a tile's recurrence.  f is the
-// lane's chunk map; (p_in, acc_in) enters lane 0 (UP, forward) or lane 31
-// (backward).  Two short scans replace one over 5-component maps: first the
-// column sums that cross lanes (a segmented sum of E, reset by lanes holding
-// a row: D == 0), then the affine recurrence p' = A p + (B acc + C) with
-// those sums folded in.
-// Predicated in-place fp64 updates (plain selects would cost two 32-bit
+// Predicated in-place fp64 update (plain selects would cost two 32-bit
 // selects per value on top of the arithmetic).
-__device__ __forceinline__ void p_add(bool p, double &c, double a) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q add.rn.f64 %0, %1, %0;\n\t}"
-      : "+d"(c) : "d"(a), "r"((int)p));
-}
 __device__ __forceinline__ void p_fma_mul(bool p, double &c, double &a, double co, double ao) {
   // if p: c = a * co + c; a = a * ao (c first: it uses the old a)
   asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t@q fma.rn.f64 %0, %1, %2, %0;\n\t"
       "@q mul.rn.f64 %1, %1, %3;\n\t}"
       : "+d"(c), "+d"(a) : "d"(co), "d"(ao), "r"((int)p));
-}
-
-template <bool UP>
-__device__ __forceinline__ void lane_states(const Tf &f, double p_in, double acc_in, double &p,
-                                            double &acc) {
-  const int lane = threadIdx.x & 31;
-  double E = f.E;
-  int D = f.D != 0.0;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const double Eo = UP ? __shfl_up_sync(0xffffffffu, E, off) : __shfl_down_sync(0xffffffffu, E, off);
-    const int Do = UP ? __shfl_up_sync(0xffffffffu, D, off) : __shfl_down_sync(0xffffffffu, D, off);
-    const bool in = UP ? lane >= off : lane + off < 32;
-    p_add(in && D, E, Eo);
-    D &= in ? Do : 1;
-  }
-  double Ex = UP ? __shfl_up_sync(0xffffffffu, E, 1) : __shfl_down_sync(0xffffffffu, E, 1);
-  int Dx = UP ? __shfl_up_sync(0xffffffffu, D, 1) : __shfl_down_sync(0xffffffffu, D, 1);
-  if (UP ? lane == 0 : lane == 31) {
-    Ex = 0.0;
-    Dx = 1;
-  }
-  acc = Dx ? __dadd_rn(acc_in, Ex) : Ex;
-  double A = f.A, C = __fma_rn(f.B, acc, f.C);
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const double Ao = UP ? __shfl_up_sync(0xffffffffu, A, off) : __shfl_down_sync(0xffffffffu, A, off);
-    const double Co = UP ? __shfl_up_sync(0xffffffffu, C, off) : __shfl_down_sync(0xffffffffu, C, off);
-    p_fma_mul(UP ? lane >= off : lane + off < 32, C, A, Co, Ao);
-  }
-  double Ax = UP ? __shfl_up_sync(0xffffffffu, A, 1) : __shfl_down_sync(0xffffffffu, A, 1);
-  double Cx = UP ? __shfl_up_sync(0xffffffffu, C, 1) : __shfl_down_sync(0xffffffffu, C, 1);
-  if (UP ? lane == 0 : lane == 31) {
-    Ax = 1.0;
-    Cx = 0.0;
-  }
-  p = __fma_rn(Ax, p_in, Cx);
 }
 
 // Max / min over the warp of non-negative doubles (no NaN): the IEEE bit
