@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_pre(SqArgs a) {
   const long long w = (long long)blockIdx.x * WPC + (threadIdx.x >> 5);
   if (w >= (long long)a.lines * a.tl) return;
   const int p = (int)(w / a.tl), t = (int)(w % a.tl);
+  griddep_wait();  // (programmatic dependent launch: the input is the previous sweep's output)
   const size_t rec = a.shared || a.D ? (size_t)t : (size_t)w;
   const double2 *W = a.W + rec * SQW;
   const double2 *D = a.D ? a.D + (size_t)w * SQW : nullptr;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_pre(SqArgs a) {
     nd->tf = Tf{s.x, 0.0, cf, 1.0, 0.0};
     nd->tb = Tf{s.y, 0.0, cb, 1.0, 0.0};
   }
+  griddep_launch();
 }
 
 // Exclusive maps of every tile along its line (warp per line, chunks of 32
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_scan(SqArgs a) {
   const int lane = threadIdx.x & 31;
   const int p = blockIdx.x * WPC + (threadIdx.x >> 5);
   if (p >= a.lines) return;
+  griddep_wait();
   Node *lv = a.nodes + (size_t)p * a.tl;
   const int n = a.tl, nch = (n + 31) / 32;
   Tf cf = tf_id(), cb = tf_id();
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_scan(SqArgs a) {
     if (have) lv[lt].xb = tf_cat_g(cb, xb);
     cb = tf_cat_g(cb, totb);
   }
+  griddep_launch();
 }
 
 // The sweep: CTA = tile t of WPC consecutive lines; lane l walks points
@@ -277,6 +281,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
   __shared__ double so[WPC][SQX];  // input staging, then the tile's outputs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x % a.tl, p0 = (blockIdx.x / a.tl) * WPC, p = p0 + warp;
+  griddep_wait();
   if (p < a.lines) {
     const size_t tile = (size_t)p * a.tl + t;
     const size_t rec = a.shared || a.D ? (size_t)t : tile;
@@ -350,6 +355,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
       const int i = k / WPC, w = k % WPC;
       if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = so[w][i];
     }
+    griddep_launch();
     return;
   }
   // the grid's scaling update on the same addresses (k_epi2d's rules,
@@ -389,6 +395,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
     a.esc[idx] = nv;
   }
   epi_block_part(err, vmax, vmin, fail, a.epart + blockIdx.x);
+  griddep_launch();
 }
 
 }  // namespace fb
