@@ -155,11 +155,14 @@ def run_2d(args, cfg, wl, world=1, rank=0):
     for _ in range(max(1, min(args.warmup, 2))):
         run()
     loops, walls = [], []
+    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
     for _ in range(args.steps):
         t0 = time.perf_counter()
         sol = run()
         walls.append(time.perf_counter() - t0)
         loops.append(sol.wall_time - sol.setup_time)
+    ck = clocks.stop()
     loop = statistics.median(loops)
     if rank != 0:
         return
@@ -192,7 +195,7 @@ def run_2d(args, cfg, wl, world=1, rank=0):
                 "h2d_bytes_per_step": 8 * (2 * pts + 2 * x1.size + 2 * y1.size),
                 "d2h_bytes_per_step": 8 * 4 * pts},
         "iterations_run": sol.iterations_run, "absorbs": sol.absorb_iterations,
-        "cost": sol.cost,
+        "cost": sol.cost, "clocks": ck, "loops_ms": [round(1e3 * x, 2) for x in loops],
     }
     print(json.dumps(line), flush=True)
 
