@@ -203,6 +203,41 @@ def test_batched_mixed_sizes_vs_oracle():
         assert abs(sol.cost - r["cost"]) <= TOL * abs(r["cost"])
 
 
+@pytest.mark.parametrize("while_loop", ["1", "0"])
+def test_batched_tol_stops_per_problem(monkeypatch, while_loop):
+    """tol > 0 on a batch whose problems converge at different iterations (and
+    one that never does): every problem keeps its own iteration count,
+    convergence flag and history while the device loop runs until the last
+    one finishes (WHILE-node graph, and the host-replayed chunk graph)."""
+    monkeypatch.setenv("FB_WHILE1D", while_loop)
+    O = _oracle()
+    rng = np.random.default_rng(23)
+    xs, ys, us, vs = [], [], [], []
+    for p in range(5):
+        n = int(rng.integers(300, 1500))
+        xs.append(np.sort(rng.uniform(0, 1, n)))
+        ys.append(np.sort(rng.uniform(0, 1, n + 17)))
+        uu, vv = rng.random(n) + 0.05, rng.random(n + 17) + 0.05
+        us.append(uu / uu.sum())
+        vs.append(vv / vv.sum())
+    es = [0.5, 0.3, 0.2, 0.15, 0.004]  # converge at 12, 19, 34, 54 and never (oracle)
+    cfg = fb.SolverConfig(epsilon=1.0, itr_max=90, tol=1e-10, stabilize=True,
+                          absorb_threshold=30.0)
+    sols = fb.sinkhorn_1d_batched([fb.Mesh1D(z) for z in xs], [fb.Mesh1D(z) for z in ys],
+                                  [fb.Measure(z) for z in us], [fb.Measure(z) for z in vs], cfg,
+                                  epsilons=es)
+    its = []
+    for p, sol in enumerate(sols):
+        r = O.sinkhorn_1d(xs[p], ys[p], us[p], vs[p], es[p], 90, 1e-10, True, 30.0)
+        assert sol.iterations_run == r["iterations"] and sol.converged == r["converged"], p
+        assert list(sol.absorb_iterations) == list(r["absorb_its"])
+        assert rel_inf(sol.phi, r["phi"]) < TOL and rel_inf(sol.psi, r["psi"]) < TOL
+        errs = [e for _, e in sol.marginal_error_history]
+        assert hist_ok(errs, r["hist"]) <= 1.0
+        its.append(sol.iterations_run)
+    assert len(set(its)) > 2 and max(its) == 90 and min(its) < 90, its
+
+
 def test_adapter_protocol_under_driver():
     """GpuAdapter1D driven by the reference-semantics host loop (solver.py:156-199)."""
     O = _oracle()
