@@ -198,3 +198,26 @@ def test_2d_loop_variants_agree(monkeypatch, env):
     tol = 0.0 if "FB_GRAPH2D" in env else 1e-12
     assert rel_inf(alt.phi, base.phi) <= tol and rel_inf(alt.psi, base.psi) <= tol
     assert abs(alt.cost - base.cost) <= max(tol, 1e-15) * abs(base.cost)
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_2d_failure_diagnostics_vs_oracle(monkeypatch, graph):
+    """ZERO_DENOM / NONFINITE in the 2D loop raise the reference's exceptions
+    with its messages, at the oracle's iteration (device-looped graph and the
+    host-stepped loop)."""
+    monkeypatch.setenv("FB_GRAPH2D", graph)
+    from oracle import oracle as O
+    cases = [  # (source x, y, target x, y, eps, exception, oracle status)
+        ([0.0, 0.5], [0.0, 0.5], [0.0, 50.0], [0.0, 50.0], 0.01, fb.ZeroDenominator, 1),
+        ([0.0], [0.0], [713.0], [0.0], 1.0, fb.NonFiniteIterate, 2),
+    ]
+    for x1, y1, x2, y2, eps, exc, st in cases:
+        x1, y1, x2, y2 = (np.array(z, dtype=float) for z in (x1, y1, x2, y2))
+        U = np.full((x1.size, y1.size), 1.0 / (x1.size * y1.size))
+        V = np.full((x2.size, y2.size), 1.0 / (x2.size * y2.size))
+        r = O.sinkhorn_2d(x1, y1, x2, y2, U, V, eps, 10, 0.0, False)
+        assert r["status"] == st
+        cfg = fb.SolverConfig(epsilon=eps, itr_max=10, tol=0.0)
+        with pytest.raises(exc) as info:
+            fb.sinkhorn_2d(_grid(x1, y1), _grid(x2, y2), fb.Measure2D(U), fb.Measure2D(V), cfg)
+        assert "enable stabilization or increase epsilon" in str(info.value)
