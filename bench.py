@@ -393,6 +393,26 @@ def main():
                "h2d_bytes_per_step": 8 * 2 * (NX + NY), "d2h_bytes_per_step":
                8 * (2 * NX + 2 * NY + itr + 5 + 1), "cost": sol.cost,
                "path": "paper_2605_26659_b200.sinkhorn_1d (host numpy in/out, incl. W1 cost)"}
+    elif cfg == 5 and os.environ.get("FINOM_E2E5", "1") != "0":
+        # this rank's share of the batch through the public batched API: plan,
+        # H2D of every problem's arrays, loop, W1 costs, D2H into per-problem Solutions
+        ms = [fb.Mesh1D(z) for z in wl["xs"]]
+        mt = [fb.Mesh1D(z) for z in wl["ys"]]
+        mu = [fb.Measure(z) for z in wl["us"]]
+        mv = [fb.Measure(z) for z in wl["vs"]]
+        scfg = fb.SolverConfig(epsilon=1.0, itr_max=itr, tol=0.0, stabilize=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sols = fb.sinkhorn_1d_batched(ms, mt, mu, mv, scfg, epsilons=wl["eps"])
+        dt = time.perf_counter() - t0
+        tdt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(tdt, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": pts_all * itr / float(tdt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * 2 * (NX + NY),
+               "d2h_bytes_per_step": 8 * (2 * NX + 2 * NY) + 8 * len(sols) * (itr + 6),
+               "path": "paper_2605_26659_b200.sinkhorn_1d_batched (host numpy in, per-problem "
+                       "Solutions out, incl. W1 costs; one call, max over ranks)"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -112,6 +112,12 @@ int finom_profile1d(finom_plan1d *plan, const double *u_dev, const double *v_dev
                     int64_t iters, int stabilize, double absorb_threshold, double *hist_dev,
                     double *ms_out, void *stream);
 
+/* Host <-> device copy of one contiguous buffer through the library's pinned
+ * staging ring (host threads per 8 MB piece, pipelined DMA): dir 0 host ->
+ * device, dir 1 device -> host.  Synchronous.  (The batched API's
+ * transfers; pageable copies run at a fraction of the link rate.) */
+int finom_stage_copy(int dir, void *host, void *dev, int64_t bytes);
+
 /* Number of kernel launches one finom_solve1d call issues. */
 int64_t finom_solve1d_launches(const finom_plan1d *plan, int64_t itr_max, int stabilize);
 

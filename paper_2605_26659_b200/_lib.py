@@ -36,6 +36,7 @@ SIGNATURES = {
     "finom_profile1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_int, _c_dbl,
                                  _vp, _vp, _vp]),
     "finom_solve1d_launches": (_c_i64, [_vp, _c_i64, _c_int]),
+    "finom_stage_copy": (_c_int, [_c_int, _vp, _vp, _c_i64]),
     "finom_sinkhorn1d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _vp, _vp, _c_dbl, _c_i64,
                                        _c_dbl, _c_int, _c_dbl, _vp, _vp, _vp, _vp, _vp, _vp,
                                        _vp, _vp, _vp]),
@@ -78,6 +79,13 @@ def load(require_device=True):
         if not torch.cuda.is_available():
             raise DeviceError("no CUDA device visible; the FINOM B200 path has no CPU fallback")
     return _lib
+
+
+def stage_copy(direction, host, dev):
+    """Contiguous host numpy array <-> device tensor through the library's pinned
+    staging (finom_stage_copy; direction 0: host -> device, 1: device -> host)."""
+    assert host.flags["C_CONTIGUOUS"] and host.nbytes == dev.numel() * dev.element_size()
+    check(load().finom_stage_copy(direction, ptr(host), ptr(dev), host.nbytes), "finom_stage_copy")
 
 
 def tile_partition(x, y):

@@ -11,7 +11,7 @@ adapter protocol (solver.py:1-16) and accepts the GPU adapter
 """
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 from time import perf_counter
 from typing import Optional
 
@@ -105,12 +105,12 @@ def raise_status(status):
 
 def history_from(errs, iterations, converged, config):
     """Apply the reference's recording cadence (solver.py:185-192) to per-iteration errors."""
-    hist = []
-    for it in range(1, iterations + 1):
-        if it % config.check_every == 0 or it == config.itr_max:
-            hist.append((it, float(errs[it - 1])))
+    its = np.arange(1, iterations + 1)
+    keep = (its % config.check_every == 0) | (its == config.itr_max)
+    vals = np.asarray(errs[:iterations], dtype=np.float64)
+    hist = list(zip(its[keep].tolist(), vals[keep].tolist()))
     if converged and (not hist or hist[-1][0] != iterations):
-        hist.append((iterations, float(errs[iterations - 1])))
+        hist.append((iterations, float(vals[iterations - 1])))
     return hist
 
 
@@ -261,8 +261,12 @@ class BatchSolver1D:
         self.P = self.plan.P
         self.eps = np.array(eps)
         f64 = dict(dtype=torch.float64, device=dev)
-        self.u = torch.from_numpy(np.concatenate([wts(u) for u in us])).to(dev)
-        self.v = torch.from_numpy(np.concatenate([wts(v) for v in vs])).to(dev)
+        hu = np.concatenate([wts(u) for u in us])
+        hv = np.concatenate([wts(v) for v in vs])
+        self.u = torch.empty(hu.size, dtype=torch.float64, device=dev)
+        self.v = torch.empty(hv.size, dtype=torch.float64, device=dev)
+        _lib.stage_copy(0, hu, self.u)
+        _lib.stage_copy(0, hv, self.v)
         NX, NY = self.u.numel(), self.v.numel()
         self.phi = torch.empty(NX, **f64)
         self.psi = torch.empty(NY, **f64)
@@ -315,32 +319,41 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
     loop = perf_counter() - t1
     raise_status(status)
     bs.compute_cost()
-    hist = bs.hist.view(bs.P, -1).cpu().numpy()
-    abs_its = bs.abs_its.view(bs.P, -1).cpu().numpy()
+    import torch
+    torch.cuda.synchronize()
+
+    def host(t):  # device tensor -> host through the pinned staging
+        h = np.empty(t.numel(), dtype=np.float64 if t.dtype == torch.float64 else np.int64)
+        _lib.stage_copy(1, h, t)
+        return h
+
+    hist = host(bs.hist).reshape(bs.P, -1)
+    abs_its = host(bs.abs_its).reshape(bs.P, -1)
     cost = bs.cost.cpu().numpy()
-    phi, psi = bs.phi.cpu().numpy(), bs.psi.cpu().numpy()
-    a, b = bs.a.cpu().numpy(), bs.b.cpu().numpy()
+    phi, psi, a, b = host(bs.phi), host(bs.psi), host(bs.a), host(bs.b)
     xo, yo = bs.plan.xoff, bs.plan.yoff
+    # Per-problem Solutions share the batch's host buffers: phi/psi/a/b are
+    # disjoint views (no copies), histories are built vectorized.
     sols = []
+    info_l = info.tolist()
+    cost_l = cost.tolist()
     for p in range(bs.P):
         x = xs[p] if hasattr(xs[p], "nodes") else None
         y = ys[p] if hasattr(ys[p], "nodes") else None
         sl, tl = slice(xo[p], xo[p + 1]), slice(yo[p], yo[p + 1])
-        cfg = SolverConfig(epsilon=float(bs.eps[p]), itr_max=config.itr_max, tol=config.tol,
-                           stabilize=config.stabilize, absorb_threshold=config.absorb_threshold,
-                           check_every=config.check_every, plan_cap=config.plan_cap)
+        e = float(bs.eps[p])
+        cfg = config if e == config.epsilon else replace(config, epsilon=e)
+        ap, bp = a[sl], b[tl]
         op = None
         if x is not None and y is not None:
-            op0 = kernel1d.build_operator(x, y, cfg.epsilon)
-            op = kernel1d.KernelOperator1D(x, y, op0.epsilon, a[sl].copy(), b[tl].copy(),
-                                           op0._plans)
-        its, conv = int(info[p, 0]), bool(info[p, 1])
+            op = kernel1d.KernelOperator1D(x, y, e, ap, bp, kernel1d._PlanCache(x, y, e))
+        its, conv, _, nab, _ = info_l[p]
         sols.append(Solution(
-            phi=phi[sl].copy(), psi=psi[tl].copy(), a=a[sl].copy(), b=b[tl].copy(), kernel=op,
-            iterations_run=its, converged=conv,
-            marginal_error_history=history_from(hist[p], its, conv, cfg),
-            wall_time=setup + loop, setup_time=setup, cost=float(cost[p]), config=cfg,
-            absorb_iterations=[int(k) for k in abs_its[p, :int(info[p, 3])]]))
+            phi=phi[sl], psi=psi[tl], a=ap, b=bp, kernel=op,
+            iterations_run=its, converged=bool(conv),
+            marginal_error_history=history_from(hist[p], its, bool(conv), cfg),
+            wall_time=setup + loop, setup_time=setup, cost=cost_l[p], config=cfg,
+            absorb_iterations=abs_its[p, :nab].tolist()))
     return sols
 
 
