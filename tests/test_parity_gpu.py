@@ -238,6 +238,31 @@ def test_batched_tol_stops_per_problem(monkeypatch, while_loop):
     assert len(set(its)) > 2 and max(its) == 90 and min(its) < 90, its
 
 
+def test_batched_many_problems_vs_oracle():
+    """A batch large enough for the host-threaded per-problem tiling (>= 64
+    problems): every problem matches its own oracle run."""
+    O = _oracle()
+    rng = np.random.default_rng(31)
+    xs, ys, us, vs, es = [], [], [], [], []
+    for p in range(70):
+        n, m = int(rng.integers(20, 400)), int(rng.integers(20, 400))
+        xs.append(np.sort(rng.uniform(0, 1, n)))
+        ys.append(np.sort(rng.uniform(0, 1, m)))
+        uu, vv = rng.random(n) + 1e-3, rng.random(m) + 1e-3
+        us.append(uu / uu.sum())
+        vs.append(vv / vv.sum())
+        es.append(float(10 ** rng.uniform(-2.5, -1)))
+    cfg = fb.SolverConfig(epsilon=1.0, itr_max=60, tol=0.0, stabilize=True, absorb_threshold=20.0)
+    sols = fb.sinkhorn_1d_batched([fb.Mesh1D(z) for z in xs], [fb.Mesh1D(z) for z in ys],
+                                  [fb.Measure(z) for z in us], [fb.Measure(z) for z in vs], cfg,
+                                  epsilons=es)
+    for p, sol in enumerate(sols):
+        r = O.sinkhorn_1d(xs[p], ys[p], us[p], vs[p], es[p], 60, 0.0, True, 20.0)
+        assert list(sol.absorb_iterations) == list(r["absorb_its"]), p
+        assert rel_inf(sol.phi, r["phi"]) < TOL and rel_inf(sol.psi, r["psi"]) < TOL, p
+        assert abs(sol.cost - r["cost"]) <= TOL * abs(r["cost"]), p
+
+
 def test_adapter_protocol_under_driver():
     """GpuAdapter1D driven by the reference-semantics host loop (solver.py:156-199)."""
     O = _oracle()
