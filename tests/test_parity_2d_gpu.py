@@ -99,11 +99,11 @@ def test_config4_full_vs_reference_pins():
     assert q["hist"] < 1 and q["phi"] < TOL and q["psi"] < TOL and q["cost"] < TOL, q
 
 
-def _sharded_case(n, m1, m2, eps, itr, seed, zero_rows=False, thr=200.0):
+def _sharded_case(n, m1, m2, eps, itr, seed, zero_rows=False, thr=200.0, square_y=False):
     rng = np.random.default_rng(seed)
     x = W.gap_mesh(rng, n, 0.1, 1.9)
     y1 = W.gap_mesh(rng, m1, 0.1, 1.9)
-    y2 = W.gap_mesh(rng, m2, 0.1, 1.9)
+    y2 = y1.copy() if square_y else W.gap_mesh(rng, m2, 0.1, 1.9)
     U = W.blobs(x, y1, rng, 8)
     V = W.blobs(x, y2, rng, 8)
     if zero_rows:  # zero-mass stretches across the shard boundaries (np.interp fill)
@@ -116,15 +116,20 @@ def _sharded_case(n, m1, m2, eps, itr, seed, zero_rows=False, thr=200.0):
     return x, y1, y2, U, V, cfg
 
 
-@pytest.mark.parametrize("R,zero,thr,m2", [(2, False, 200.0, 40), (3, True, 30.0, 40),
-                                           (4, False, 30.0, 52)])
-def test_row_sharded_2d_vs_oracle(R, zero, thr, m2):
+@pytest.mark.parametrize("R,zero,thr,m2,sq", [(2, False, 200.0, 40, False),
+                                              (3, True, 30.0, 40, False),
+                                              (4, False, 30.0, 52, False),
+                                              (2, False, 30.0, 300, True),
+                                              (3, True, 30.0, 300, True)])
+def test_row_sharded_2d_vs_oracle(R, zero, thr, m2, sq):
     """SURVEY 8(e) config-4 decomposition: R row shards with carry exchange
     (run one after another on one GPU, collectives as concatenation) against
-    the oracle of the unsharded reference algorithm."""
+    the oracle of the unsharded reference algorithm.  sq: source y == target
+    y (config 4's shape), so the shard-local y sweeps take the square path."""
     from oracle import oracle as O
     from paper_2605_26659_b200 import sharding as S
-    x, y1, y2, U, V, cfg = _sharded_case(96, 40, m2, 2e-3, 50, 11 + R, zero, thr)
+    m1 = m2 if sq else 40
+    x, y1, y2, U, V, cfg = _sharded_case(96, m1, m2, 2e-3, 50, 11 + R, zero, thr, square_y=sq)
     src, tgt = _grid(x, y1), _grid(x.copy(), y2)
     sol = S.sinkhorn_2d_row_sharded_sim(src, tgt, fb.Measure2D(U), fb.Measure2D(V), cfg, R)
     r = O.sinkhorn_2d(x, y1, x, y2, U, V, cfg.epsilon, cfg.itr_max, 0.0, True, thr)
