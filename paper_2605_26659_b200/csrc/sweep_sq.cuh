@@ -91,6 +91,7 @@ struct SqArgs {
   double *esc;
   EpiPart *epart;
   int eerr;
+  int ek0, eng;           // failure indices: row shard [ek0, ..) of eng grid rows (0, lines: whole grid)
 };
 
 // Records of one tile (warp per (line, tile); shared records: line 0 only).
@@ -378,15 +379,17 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
     const int k = threadIdx.x + q * NTHR, i = k / WPC, w = k % WPC;
     if (k >= cnt * WPC || p0 + w >= a.lines) continue;
     const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+    // flat index of the whole grid (a row shard holds rows [ek0, ek0 + lines) of eng)
+    const long long kg = a.ek0 + p0 + w + (long long)a.eng * (t * SQT + i);
     const double wv = wq[q], tt = so[w][i];
     if (a.eerr) err = __dadd_rn(err, fabs(__dsub_rn(__dmul_rn(sq[q], tt), wv)));
     double nv;
     if (tt == 0.0) {
-      if (wv > 0.0) fail = min(fail, (idx << 2) | ST_ZD);
+      if (wv > 0.0) fail = min(fail, (kg << 2) | ST_ZD);
       nv = 0.0;
     } else {
       nv = __ddiv_rn(wv, tt);
-      if (!isfinite(nv)) fail = min(fail, (idx << 2) | ST_NF);
+      if (!isfinite(nv)) fail = min(fail, (kg << 2) | ST_NF);
       else if (wv > 0.0) {
         vmax = fmax(vmax, nv);
         vmin = fmin(vmin, nv);
