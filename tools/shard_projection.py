@@ -18,14 +18,16 @@ for R in (1, 2, 4, 8):
     times = []
     for k, s in enumerate(shards):
         for half in (0, 1):  # warm
-            seg = torch.cat([s.xpre(half, False).clone() for _ in range(R)])
+            seg0 = s.xpre(half, False).clone()
+            seg = torch.cat([seg0] * R)
             s.finish(half, False, seg, R, k)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(its):
             for half in (0, 1):
-                seg = torch.cat([s.xpre(half, False).clone() for _ in range(R)])
+                seg0 = s.xpre(half, False).clone()
+                seg = torch.cat([seg0] * R)
                 s.finish(half, False, seg, R, k)
         e1.record(); torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / its)
