@@ -92,6 +92,11 @@ struct SqArgs {
   EpiPart *epart;
   int eerr;
   int ek0, eng;           // failure indices: row shard [ek0, ..) of eng grid rows (0, lines: whole grid)
+  // row-shard window (the x sweeps of a shard): the lines are the segment
+  // [k0, k0 + n) of lines of the whole mesh (Z already offset by k0)
+  int k0;
+  const double *carry;    // nullable: per line incoming (p, acc, q, accb) from the other shards
+  double *tot;            // nullable: per line segment totals (forward Tf, backward Tf)
 };
 
 // Records of one tile (warp per (line, tile); shared records: line 0 only).
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_build(SqArgs a) {
     rho[k] = 1.0; del[k] = 0.0; sig[k] = 1.0; mu[k] = 0.0;  // padding: identity steps
     if (r < a.n) {
       del[k] = exp(__dmul_rn(__dadd_rn(A(r), B(r)), a.inv));
-      if (r > 0)
+      if (r > 0 || a.k0 > 0)  // (a window's first point: the mesh point before it is a.Z[-1])
         rho[k] = exp(__dmul_rn(__dadd_rn(-(a.Z[r] - a.Z[r - 1]), __dsub_rn(A(r), A(r - 1))), a.inv));
       if (r + 1 < a.n) {
         const double g = a.Z[r + 1] - a.Z[r];
@@ -260,6 +265,7 @@ __global__ void __launch_bounds__(NTHR) k_sq_scan(SqArgs a) {
       if (nch == 1) lv[lt].xb = xb;
     }
     cf = tf_cat_g(cf, totf);
+    if (nch == 1) cb = totb;
   }
   for (int c = nch - 1; nch > 1 && c >= 0; --c) {
     const int lt = 32 * c + lane;
@@ -270,7 +276,36 @@ __global__ void __launch_bounds__(NTHR) k_sq_scan(SqArgs a) {
     if (have) lv[lt].xb = tf_cat_g(cb, xb);
     cb = tf_cat_g(cb, totb);
   }
+  if (a.tot && lane == 0) {  // the line segment's totals (row shards: k_sq_seg_tot)
+    double *o = a.tot + 10 * (size_t)p;
+    o[0] = cf.A; o[1] = cf.B; o[2] = cf.C; o[3] = cf.D; o[4] = cf.E;
+    o[5] = cb.A; o[6] = cb.B; o[7] = cb.C; o[8] = cb.D; o[9] = cb.E;
+  }
   griddep_launch();
+}
+
+// A row shard's exported segment totals (k_seg_carry's input, 10 doubles per
+// line): the forward total as is; the backward total extended by the step
+// into the last row of the shard before (row k0 - 1 of the whole mesh):
+// Q_{k0-1} = sigma_{k0-1} Q_{k0} + mu_{k0-1} v_{k0}, with k_sq_build's
+// exponent expressions (alpha = 0, beta = this line's shifts).
+__global__ void k_sq_seg_tot(SqArgs a, double *out) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < a.lines; p += gridDim.x * blockDim.x) {
+    const double *t = a.tot + 10 * (size_t)p;
+    double *o = out + 10 * (size_t)p;
+    for (int k = 0; k < 5; ++k) o[k] = t[k];
+    double A = t[5], C = t[7];
+    if (a.k0 > 0) {
+      const double g = a.Z[0] - a.Z[-1];
+      const double be = a.beta ? a.beta[(size_t)p * a.n] : 0.0;
+      const double sig = exp(__dmul_rn(__dadd_rn(-g, __dsub_rn(0.0, 0.0)), a.inv));
+      const double mu = exp(__dmul_rn(__dadd_rn(-g, __dadd_rn(0.0, be)), a.inv));
+      const double v0 = a.vin[(size_t)p * a.n];
+      A = gm(sig, A);
+      C = __dadd_rn(gm(sig, C), __dmul_rn(mu, v0));
+    }
+    o[5] = A; o[6] = t[6]; o[7] = C; o[8] = t[8]; o[9] = t[9];
+  }
 }
 
 // The sweep: CTA = tile t of WPC consecutive lines; lane l walks points
@@ -306,8 +341,16 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
     double x[EPT + 1];
     sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, so[warp], x);
     double pin = 0.0, qin = 0.0;  // the tile's incoming P (lane 0) / Q (lane 31)
-    if (lane == 0) pin = __ldcg(&a.nodes[tile].xf.C);
-    if (lane == 31) qin = __ldcg(&a.nodes[tile].xb.C);
+    // (the tile's exclusive maps applied to the line's incoming states: zero,
+    // or a row shard's carries from the other shards, as tf_apply_g)
+    if (lane == 0) {
+      const double cp = a.carry ? __ldg(a.carry + 4 * (size_t)p) : 0.0;
+      pin = (gm(__ldcg(&a.nodes[tile].xf.A), cp) + 0.0) + __ldcg(&a.nodes[tile].xf.C);
+    }
+    if (lane == 31) {
+      const double cq = a.carry ? __ldg(a.carry + 4 * (size_t)p + 2) : 0.0;
+      qin = (gm(__ldcg(&a.nodes[tile].xb.A), cq) + 0.0) + __ldcg(&a.nodes[tile].xb.C);
+    }
     // lane maps: forward P_end = af P_in + cf, backward Q_first = ab Q_after + cb
     double af = 1.0, cf = 0.0, ab = 1.0, cb = 0.0;
 #pragma unroll
