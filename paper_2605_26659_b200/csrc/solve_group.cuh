@@ -1,0 +1,347 @@
+// solve_group.cuh -- the whole 1D solve loop of a batch in ONE persistent
+// kernel, a group of warps per problem (included by finom_1d.cu).
+//
+// Batches of independent problems (config 5: 8192 x 16384) need no
+// communication between problems, so a problem's every iteration can run
+// inside one group of g warps of one CTA (g = 1 for large batches):
+//   * the carries of a half come from the tile maps the previous half's
+//     epilogue wrote (tile_compute), composed by the group itself (lane
+//     chunks, warp scan, the group's other warps through shared memory) into
+//     per-tile incoming states -- no resolve tree, no k_resolve launch;
+//   * the partials (marginal error, extremes, failure) are reduced in tile
+//     order as the warp walks its tiles, then across the group's warps in
+//     warp order (deterministic), and run_driver's bookkeeping
+//     (solver.py:173-198) runs in registers of every warp of the group;
+//   * an absorption (solver._shift + kernel1d.absorb) rebuilds the group's
+//     tile records in place (absorb_core) -- no k_absorb launch;
+//   * problems are taken from a queue (one atomic per problem), so a batch of
+//     equal problems keeps every SM busy until the tail.
+// The per-tile work (bulk-copied record, one-state walk, epilogue) is the
+// k_step code; only the carry source and the bookkeeping differ.
+#pragma once
+
+namespace fb {
+
+constexpr int GW = 16;                  // warps per CTA
+constexpr int GTHR = 32 * GW;
+constexpr int WREG = WST > WSM ? WST : WSM;  // shared doubles per warp (step / absorb)
+
+struct GroupArgs {
+  Dev d;
+  double *S4;       // per tile: incoming (p, acc, q, accb) of the current half
+  int *queue;       // [0]: next problem
+  int g;            // warps per problem (1, 2, 4, 8, 16)
+  double *a_out, *b_out;
+  long long *info;
+};
+
+// One group's exchange slots in shared memory: per warp the chunk aggregates
+// of both directions and the partials (err, max, min, fail).
+struct GX {
+  Tf f, b;
+  double part[4];
+  int prob, pad;
+};
+
+__device__ __forceinline__ void group_sync(int id, int nthr) {
+  if (nthr == 32) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");
+}
+
+// Per-tile incoming states of one half for tiles [b, e) of the warp (the
+// warp's share of its problem): lane chunks composed sequentially, a warp
+// scan, the group's other warps' totals (shared memory), then per-tile states
+// into S4 (lane-sequential).  Maps: R.lev[0] (written by the previous half's
+// epilogue or by the table build), forward composed left to right, backward
+// right to left; guarded compositions (a structural zero stays zero).
+__device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, int e, int j,
+                                              int g, GX *gx, int bar, int lane) {
+  const Node *nd = R.lev[0];
+  const int n = e - b;
+  const int L = (n + 31) / 32;
+  const int lb = min(b + lane * L, e), le = min(lb + L, e);
+  Tf f = tf_id(), bk = tf_id();
+  for (int t = lb; t < le; ++t) f = tf_cat_g(f, ldcg_tf(&nd[t].tf));
+  for (int t = le - 1; t >= lb; --t) bk = tf_cat_g(bk, ldcg_tf(&nd[t].tb));
+  Tf xf, xb, totf, totb;
+  warp_scan2<true>(f, bk, xf, xb, totf, totb);
+  double p = 0.0, acc = 0.0, q = 0.0, accb = 0.0;
+  if (g > 1) {
+    if (lane == 0) {
+      gx[j].f = totf;
+      gx[j].b = totb;
+    }
+    group_sync(bar, 32 * g);
+    // the totals of the group's earlier warps (forward) and later warps
+    // (backward), applied to the problem's zero boundary states
+    for (int k = 0; k < j; ++k) tf_apply_g(gx[k].f, p, acc);
+    for (int k = g - 1; k > j; --k) tf_apply_g(gx[k].b, q, accb);
+    group_sync(bar, 32 * g);  // (gx is rewritten by the partials below)
+  }
+  tf_apply_g(xf, p, acc);
+  tf_apply_g(xb, q, accb);
+  for (int t = lb; t < le; ++t) {
+    S4[4 * (size_t)t] = p;
+    S4[4 * (size_t)t + 1] = acc;
+    tf_apply_g(ldcg_tf(&nd[t].tf), p, acc);
+  }
+  for (int t = le - 1; t >= lb; --t) {
+    S4[4 * (size_t)t + 2] = q;
+    S4[4 * (size_t)t + 3] = accb;
+    tf_apply_g(ldcg_tf(&nd[t].tb), q, accb);
+  }
+  __syncwarp();
+}
+
+// L2 prefetch of [p, p + bytes) (16-byte aligned interior).
+__device__ __forceinline__ void l2_prefetch(const void *p, size_t bytes) {
+  const unsigned long long a = reinterpret_cast<unsigned long long>(p);
+  const unsigned long long a16 = (a + 15) & ~15ull, e16 = (a + bytes) & ~15ull;
+  if (e16 > a16)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a16), "r"((unsigned)(e16 - a16))
+                 : "memory");
+}
+// The next tile's record and vectors into L2 while this one computes.
+template <int HALF>
+__device__ __forceinline__ void group_prefetch(const Dev &d, int t, const TileStep &ts) {
+  const int nr = HALF == 0 ? ts.ny : ts.nx, nc = HALF == 0 ? ts.nx : ts.ny;
+  l2_prefetch(d.TR[HALF] + (size_t)t * TREC, (size_t)(((REC_KT + 3 * nr) * 8 + 15) & ~15));
+  const long long rb = HALF == 0 ? ts.yb : ts.xb, cb = HALF == 0 ? ts.xb : ts.yb;
+  if (HALF == 0) l2_prefetch(d.PSI + rb, 8 * (size_t)nr);
+  l2_prefetch((HALF == 0 ? d.PHI : d.PSI) + cb, 8 * (size_t)nc);
+}
+
+// One half step of tile t with incoming states init = S4 + 4t (the k_step
+// loads without the tree and control reads); partials to part.  nts: the
+// next tile's descriptor (prefetched into L2 during this tile), if any.
+template <int HALF>
+__device__ __forceinline__ void group_tile(const Dev &d, int t, const TileStep &ts, bool next,
+                                           const TileStep &nts, double *wsm,
+                                           unsigned long long *bar, int lane, unsigned &phase,
+                                           const double *init, double *part) {
+  TileIn in;
+  in.t = t;
+  in.nr = HALF == 0 ? ts.ny : ts.nx;
+  in.nc = HALF == 0 ? ts.nx : ts.ny;
+  in.rb = HALF == 0 ? ts.yb : ts.xb;
+  in.cb = HALF == 0 ? ts.xb : ts.yb;
+  in.r0 = HALF == 0 ? ts.y0 : ts.x0;
+  in.rec = wsm;
+  in.reset = 0;
+  const unsigned rbytes = (unsigned)(((REC_KT + 3 * in.nr) * 8 + 15) & ~15);
+  const double *Rs = (HALF == 0 ? d.PSI : d.PHI) + in.rb;
+  const double *Cs = (HALF == 0 ? d.PHI : d.PSI) + in.cb;
+  in.rold = vec_place(in.rec + TREC, Rs);
+  in.cv = vec_place(in.rold + (HALF == 0 ? in.nr : 0), Cs);
+  if (lane == 0) {
+    const VecStage vr = vec_stage(Rs, HALF == 0 ? in.nr : 0), vc = vec_stage(Cs, in.nc);
+    bulk_expect(bar, rbytes + vr.bytes + vc.bytes);
+    bulk_rec(in.rec, d.TR[HALF] + (size_t)t * TREC, rbytes, bar);
+    vec_issue(in.rold, Rs, vr, bar);
+    vec_issue(in.cv, Cs, vc, bar);
+    if (next) group_prefetch<HALF>(d, t + 1, nts);
+  }
+  // lanes 0 / 4: the incoming states (forward / backward), off the walk's path
+  double st0 = 0.0, st1 = 0.0;
+  if (lane == 0 || lane == 4) {
+    st0 = __ldcg(init + (lane == 0 ? 0 : 2));
+    st1 = __ldcg(init + (lane == 0 ? 1 : 3));
+  }
+  cp_async_wait();
+  bar_wait(bar, phase & 1u);
+  ++phase;
+  __syncwarp();
+#ifdef FB_DBG_PHASE
+  long long ph_t0 = 0;
+  tile_compute<HALF, true>(d, in, tf_id(), lane, ph_t0, nullptr, part, true, st0, st1);
+#else
+  tile_compute<HALF, true>(d, in, tf_id(), lane, nullptr, part, true, st0, st1);
+#endif
+}
+
+// Partials of the warp's tiles (in tile order) -> the group's (in warp order).
+__device__ __noinline__ void group_partials(double (&pw)[4], int j, int g, GX *gx, int bar,
+                                               int lane) {
+  if (g == 1) return;
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) gx[j].part[k] = pw[k];
+  group_sync(bar, 32 * g);
+  double e = 0.0, mx = 0.0, mn = INFINITY, fl = -1.0;
+  for (int k = 0; k < g; ++k) {
+    e = __dadd_rn(e, gx[k].part[0]);
+    mx = fmax(mx, gx[k].part[1]);
+    mn = fmin(mn, gx[k].part[2]);
+    fl = fmax(fl, gx[k].part[3]);
+  }
+  pw[0] = e;
+  pw[1] = mx;
+  pw[2] = mn;
+  pw[3] = fl;
+  group_sync(bar, 32 * g);
+}
+
+// The table (re)build of the warp's tiles, out of line: it runs at the start
+// of a problem and on absorptions only, and keeps the hot loop's code small
+// (the instruction cache holds the two half steps).
+__device__ __noinline__ void group_build(const Dev &d, int build, int b, int e, double *wsm,
+                                         const double2 *tab, int sb, bool had) {
+  for (int t = b; t < e; ++t) {
+    absorb_core(d, build, t, wsm, tab, sb, had);
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double2 tab[64];
+  __shared__ GX gxs[GW];
+  __shared__ int gprob[GW];
+  __shared__ unsigned long long mbar[GW];  // (absorb_core uses the whole warp region)
+  load_tab(tab);
+  __syncthreads();
+  const Dev &d = a.d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = a.g, j = warp % g, grp = warp / g;
+  const int bar = 1 + grp;  // named barrier of the group (g > 1)
+  GX *gx = gxs + grp * g;
+  double *wsm = smem + (size_t)warp * WREG;
+  unsigned long long *mb = mbar + warp;
+  if (lane == 0) bar_init(mb);
+  __syncwarp();
+  unsigned phase = 0;
+  for (;;) {
+    if (j == 0 && lane == 0) gprob[grp] = atomicAdd(a.queue, 1);
+    group_sync(bar, 32 * g);
+    const int prob = gprob[grp];
+    group_sync(bar, 32 * g);
+    if (prob >= d.P) break;
+    const ProbDesc &P = d.probs[prob];
+    const int b = P.tile0 + (int)((long long)P.ntiles * j / g);
+    const int e = P.tile0 + (int)((long long)P.ntiles * (j + 1) / g);
+    // ---- solve prologue (solver.py:165-166): phi = psi = 1/n, shifts 0
+    const double h0 = 1.0 / (double)P.n;
+    if (e > b) {
+      const TileDesc t0d = d.tiles[b], t1d = d.tiles[e - 1];
+      for (int k = t0d.x0 + lane; k < t1d.x1; k += 32) {
+        d.PHI[P.xoff + k] = h0;
+        d.A[0][P.xoff + k] = 0.0;
+      }
+      for (int k = t0d.y0 + lane; k < t1d.y1; k += 32) {
+        d.PSI[P.yoff + k] = h0;
+        d.B[0][P.yoff + k] = 0.0;
+      }
+    }
+    group_sync(bar, 32 * g);
+    // tables of the initial kernel, half A's maps for the initial phi
+    group_build(d, 1, b, e, wsm, tab, 0, false);
+    group_sync(bar, 32 * g);
+    int it = 0, status = 0, fail_it = 0, sbuf = 0, n_abs = 0, converged = 0;
+    bool absorbed = false;
+    double err = 0.0, psmax = 0.0, psmin = INFINITY;
+    for (;;) {
+      // ---- half A: psi <- v / K'^T phi (_kernels.py:278-314)
+      group_carries(d.RA, a.S4, b, e, j, g, gx, bar, lane);
+      double pw[4] = {0.0, 0.0, INFINITY, -1.0};
+      TileStep ts = d.steps[b < e ? b : 0];
+      for (int t = b; t < e; ++t) {
+        double pt[4];
+        const TileStep nts = d.steps[t + 1 < e ? t + 1 : t];
+        group_tile<0>(d, t, ts, t + 1 < e, nts, wsm, mb, lane, phase, a.S4 + 4 * (size_t)t, pt);
+        ts = nts;
+        pw[0] = __dadd_rn(pw[0], pt[0]);
+        pw[1] = fmax(pw[1], pt[1]);
+        pw[2] = fmin(pw[2], pt[2]);
+        pw[3] = fmax(pw[3], pt[3]);
+      }
+      group_partials(pw, j, g, gx, bar, lane);
+      err = pw[0];
+      psmax = pw[1];
+      psmin = pw[2];
+      if (j == 0 && lane == 0) d.hist[(long long)prob * d.itr_max + it] = err;
+      if (pw[3] >= 0.0) {  // solver.py:177-184 (failure in half A)
+        const long long fl = (long long)pw[3];
+        status = (int)(fl & 3);
+        fail_it = it + 1;
+        it += 1;
+        break;
+      }
+      // ---- half B: phi <- u / K' psi (_kernels.py:315-349)
+      group_sync(bar, 32 * g);  // every psi of the problem is final
+      group_carries(d.RB, a.S4, b, e, j, g, gx, bar, lane);
+      double qw[4] = {0.0, 0.0, INFINITY, -1.0};
+      TileStep ts1 = d.steps[b < e ? b : 0];
+      for (int t = b; t < e; ++t) {
+        double pt[4];
+        const TileStep nts = d.steps[t + 1 < e ? t + 1 : t];
+        group_tile<1>(d, t, ts1, t + 1 < e, nts, wsm, mb, lane, phase, a.S4 + 4 * (size_t)t, pt);
+        ts1 = nts;
+        qw[1] = fmax(qw[1], pt[1]);
+        qw[2] = fmin(qw[2], pt[2]);
+        qw[3] = fmax(qw[3], pt[3]);
+      }
+      group_partials(qw, j, g, gx, bar, lane);
+      const double phmax = qw[1], phmin = qw[2];
+      const int k = ++it;  // solver.py:177
+      if (qw[3] >= 0.0) {
+        const long long fl = (long long)qw[3];
+        status = (int)(fl & 3);
+        fail_it = k;
+        break;
+      }
+      if (d.tol > 0.0 && err <= d.tol) {  // solver.py:188-192
+        converged = 1;
+        break;
+      }
+      if (d.stabilize && (phmax > d.hi_cut || psmax > d.hi_cut || phmin < d.lo_cut ||
+                          psmin < d.lo_cut)) {  // solver.py:193-198: absorb, phi = psi = 1
+        if (j == 0 && lane == 0 && d.absorb_its)
+          d.absorb_its[(long long)prob * d.itr_max + n_abs] = k;
+        n_abs += 1;
+        group_sync(bar, 32 * g);  // every phi of the problem is final
+        group_build(d, 0, b, e, wsm, tab, sbuf, absorbed);
+        group_sync(bar, 32 * g);  // every tile has read the old shifts and scalings
+        sbuf ^= 1;
+        absorbed = true;
+        if (e > b) {
+          const TileDesc t0d = d.tiles[b], t1d = d.tiles[e - 1];
+          for (int q = t0d.x0 + lane; q < t1d.x1; q += 32) d.PHI[P.xoff + q] = 1.0;
+          for (int q = t0d.y0 + lane; q < t1d.y1; q += 32) d.PSI[P.yoff + q] = 1.0;
+        }
+        __syncwarp();
+      }
+      if (k >= d.itr_max) break;
+      group_sync(bar, 32 * g);  // every phi / half-A map of the problem is final
+    }
+    // ---- k_final's part: shifts out, info, control block
+    const double *As = d.A[sbuf], *Bs = d.B[sbuf];
+    if (e > b) {
+      const TileDesc t0d = d.tiles[b], t1d = d.tiles[e - 1];
+      for (int q = t0d.x0 + lane; q < t1d.x1; q += 32)
+        a.a_out[P.xoff + q] = absorbed ? As[P.xoff + q] : 0.0;
+      for (int q = t0d.y0 + lane; q < t1d.y1; q += 32)
+        a.b_out[P.yoff + q] = absorbed ? Bs[P.yoff + q] : 0.0;
+    }
+    if (j == 0 && lane == 0) {
+      long long *inf = a.info + 5 * (long long)prob;
+      inf[0] = it;
+      inf[1] = converged;
+      inf[2] = status;
+      inf[3] = n_abs;
+      inf[4] = fail_it;
+      Ctl c{};
+      c.it = it;
+      c.done = 1;
+      c.status = status;
+      c.fail_it = fail_it;
+      c.absorbed = absorbed;
+      c.converged = converged;
+      c.n_absorb = n_abs;
+      c.sbuf = sbuf;
+      c.err = err;
+      d.ctl[prob] = c;
+    }
+    group_sync(bar, 32 * g);
+  }
+}
+
+}  // namespace fb
