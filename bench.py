@@ -1,11 +1,19 @@
 """Benchmark of the FINOM Sinkhorn hot path on B200 (driver contract).
 
-Default workload: BASELINE.json configs[1] (config 2): 1D W1 Sinkhorn, fp64,
-N = M = 2^22 graded meshes, eps = 1e-3, 200 fixed iterations, log-domain
-stabilization on (absorptions happen inside the timed loop).  One step =
-one full 200-iteration solve through the device-resident loop.
+Default workload: BASELINE.json config 5 at every GPU count (the metric is
+quoted on 1/2/4/8 B200; config 5 is the configuration that shards): a batch
+of 8192 1D W1 Sinkhorn problems, fp64, N = M = 16384 each, eps per problem
+10^U[-3,-1], 200 fixed iterations, log-domain stabilization on
+(absorptions happen inside the timed loop), the batch split by problem
+across the ranks ("scaling": "strong", no data-path collective).  One step
+= one full 200-iteration solve of the rank's problems through the device
+loop.  --config 2 is the single-GPU 1D problem (N = M = 2^22), --config
+1/3/4 the other BASELINE configs (4 row-sharded under torchrun).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 1|2|5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 1..5]
+
+--gpus N without torchrun re-executes itself under torch.distributed.run
+with N ranks (127.0.0.1); under torchrun WORLD_SIZE must equal N.
 
 value: mesh-points x iterations / s over the device loop, inputs resident
 in HBM (CUDA events on the launching stream, barrier + sync both sides, max
@@ -103,12 +111,16 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(name):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+def ncu_traffic(name, cfg):
+    """dram bytes per launch of the dominant kernel (per iteration for a
+    whole-solve kernel) from the committed ncu summary of this config."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            return json.load(f).get(name, {}).get("dram_bytes_per_launch")
+            d = json.load(f)
+        e = d.get("config%d" % cfg, {}).get(name) or (d.get(name) if cfg == 2 else None)
+        return None if e is None else e.get("dram_bytes_per_iteration",
+                                             e.get("dram_bytes_per_launch"))
     except Exception:  # noqa: BLE001
         return None
 
@@ -271,7 +283,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(loops),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if cfg in (4, 5) else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
         "config": config_json(cfg, {"batch": 8192}, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -281,15 +294,33 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def relaunch_distributed(args):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run
+    with N ranks on this node (the driver's own launch form)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch_distributed(args)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit("bench.py: WORLD_SIZE=%s but --gpus %d" % (os.environ["WORLD_SIZE"],
+                                                                  args.gpus))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -354,14 +385,8 @@ def main():
     ms_max = float(ms_t.item())
     value = pts_all * itr * args.steps / (ms_max * 1e-3)
 
-    # per-kernel timing (events around each launch) for the roofline
     lib = _lib.load()
-    prof = np.zeros(6)
-    hist_dev = torch.zeros(bs.P * itr, dtype=torch.float64, device="cuda")
-    _lib.check(lib.finom_profile1d(bs.plan.handle, _lib.ptr(bs.u), _lib.ptr(bs.v),
-                                   _lib.ptr(bs.phi), _lib.ptr(bs.psi), _lib.ptr(bs.a),
-                                   _lib.ptr(bs.b), itr, 1, 200.0, _lib.ptr(hist_dev),
-                                   _lib.ptr(prof), _lib.stream_ptr()), "finom_profile1d")
+    group = int(lib.finom_solve1d_group(bs.plan.handle))
     NX, NY = bs.u.numel(), bs.v.numel()
     # algorithmic bytes: per iteration 40n + 48m unabsorbed,
     # 56n + 64m once the problem has absorbed (shift reads), weighted by the
@@ -372,10 +397,27 @@ def main():
     first = np.where(info[:, 3] > 0, abs_its[:, 0], itr).astype(np.float64)
     alg_bytes_it = float(np.sum((40 * ns + 48 * ms_) * first
                                 + (56 * ns + 64 * ms_) * (itr - first))) / itr
-    t_half = (prof[0] + prof[1]) * 1e-3
-    achieved = alg_bytes_it / t_half / 1e9
     peak, peak_src = peaks()
     launches = int(lib.finom_solve1d_launches(bs.plan.handle, itr, 1)) * args.steps
+    prof = np.zeros(6)
+    if group:
+        # the group solve is ONE kernel (k_solve_group) for the whole loop: its
+        # duration is the timed step (CUDA events on its stream, this rank)
+        t_it = ms / args.steps / itr * 1e-3
+        kernel = ("k_solve_group (whole %d-iteration solve in one launch, %d warp(s) per "
+                  "problem)" % (itr, group))
+        traffic_key = "k_solve_group"
+    else:
+        # per-kernel timing (events around each launch) of the tile-parallel loop
+        hist_dev = torch.zeros(bs.P * itr, dtype=torch.float64, device="cuda")
+        _lib.check(lib.finom_profile1d(bs.plan.handle, _lib.ptr(bs.u), _lib.ptr(bs.v),
+                                       _lib.ptr(bs.phi), _lib.ptr(bs.psi), _lib.ptr(bs.a),
+                                       _lib.ptr(bs.b), itr, 1, 200.0, _lib.ptr(hist_dev),
+                                       _lib.ptr(prof), _lib.stream_ptr()), "finom_profile1d")
+        t_it = (prof[0] + prof[1]) * 1e-3
+        kernel = "k_step<A>+k_resolve<A>+k_step<B>+k_resolve<B>"
+        traffic_key = "k_step"
+    achieved = alg_bytes_it / t_it / 1e9
 
     e2e = None
     if rank == 0 and cfg != 5:
@@ -437,19 +479,21 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if cfg == 5 else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, BASELINE.json shapes; see DESIGN.md)",
             "config": config_json(cfg, wl, world),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": ncu_traffic("k_step") if cfg == 2 else None,
-                         "peak_source": peak_src,
-                         "kernel": "k_step<A>+k_resolve<A>+k_step<B>+k_resolve<B>",
-                         "algorithmic_bytes_per_iteration": alg_bytes_it,
-                         "bytes_rule": "88 B/pt unabsorbed, 120 B/pt absorbed (SURVEY 8d)",
-                         "ms_half_a": prof[0], "ms_half_b": prof[1],
-                         "ms_resolve": prof[2], "ms_absorb": prof[3],
-                         "ms_iteration_ungraphed": prof[4]},
+            "roofline": dict({"bound": "hbm", "achieved": achieved, "peak": peak,
+                              "unit": "GB/s", "frac": achieved / peak,
+                              "traffic": ncu_traffic(traffic_key, cfg),
+                              "peak_source": peak_src, "kernel": kernel,
+                              "algorithmic_bytes_per_iteration": alg_bytes_it,
+                              "bytes_rule": "88 B/pt unabsorbed, 120 B/pt absorbed (SURVEY 8d)",
+                              "ms_iteration": t_it * 1e3},
+                             **({} if group else {
+                                 "ms_half_a": prof[0], "ms_half_b": prof[1],
+                                 "ms_resolve": prof[2], "ms_absorb": prof[3],
+                                 "ms_iteration_ungraphed": prof[4]})),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,

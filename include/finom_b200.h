@@ -46,12 +46,20 @@ const char *finom_build_info(void);
 /* Builds the device plan for P 1D problems: uploads the meshes, computes the
  * dividing-index tile partition (kernel1d.dividing_index,
  * kernel1d.py:55-62, and the merge-path split of x U y) and allocates the
- * work buffers.  Replaces kernel1d.build_operator (kernel1d.py:234-255):
- * no kernel tables are stored; every factor is recomputed on the fly. */
+ * work buffers.  Replaces kernel1d.build_operator (kernel1d.py:234-255).
+ * The solve loop keeps per-tile kernel tables for the current absorption
+ * epoch (built on the device at solve start and rebuilt at every
+ * absorption, like the reference's assembled reps, kernel1d.py:121-159);
+ * apply / cost evaluate their factors on the fly. */
 int finom_plan1d_create(int64_t P, const int64_t *xoff_host, const double *x_host,
                         const int64_t *yoff_host, const double *y_host,
                         const double *eps_host, void *stream, finom_plan1d **plan_out);
 int finom_plan1d_destroy(finom_plan1d *plan);
+
+/* Plans and grids allocate from a library-owned memory pool that keeps up to
+ * FINOM_POOL_KEEP_GB (env, default 16) GiB of freed memory for the next
+ * plan; this returns all of it to the driver. */
+int finom_release_memory(void);
 
 /* Host-only: the merge-path tile partition of one mesh pair and the
  * merged-order masks the kernels walk (no CUDA call; for tests).  Returns the
@@ -121,6 +129,12 @@ int finom_stage_copy(int dir, void *host, void *dev, int64_t bytes);
 /* Number of kernel launches one finom_solve1d call issues. */
 int64_t finom_solve1d_launches(const finom_plan1d *plan, int64_t itr_max, int stabilize);
 
+/* Loop form finom_solve1d uses for this plan: 0 = the tile-parallel loop
+ * (k_step / k_resolve per half, device-looped graph), g > 0 = the group
+ * solve (one persistent k_solve_group launch, g warps per problem; batches
+ * that fill the GPU).  FB_GROUP=0/1 in the environment forces. */
+int finom_solve1d_group(const finom_plan1d *plan);
+
 /* End-to-end call with HOST buffers (one problem): sinkhorn_1d
  * (solver.py:202-230) including transport_cost_fast.  hist_host: itr_max
  * doubles; info_host: 5 int64 (as finom_solve1d); cost_host: 1 double.
@@ -157,6 +171,46 @@ int finom_apply2d_host(int64_t n1, const double *x1, int64_t m1, const double *y
 int finom_cost2d_host(int64_t n1, const double *x1, int64_t m1, const double *y1, int64_t n2,
                       const double *x2, int64_t m2, const double *y2, double eps, const double *A,
                       const double *B, const double *phi, const double *psi, double *cost);
+
+/* ---- 2D grids on device buffers (the plan / solve split of sinkhorn_2d) ----
+ * A grid plan holds the sweep plans, scratch grids and solve state of one
+ * (source x1[n1] x y1[m1], target x2[n2] x y2[m2], eps) -- build it once,
+ * then solve / iterate / cost on caller-owned device buffers with no
+ * allocation.  Grids are flat column-major (x fastest, mesh.py:85-107).
+ * Replaces kernel2d.build_operator_2d + _GridAdapter (kernel2d.py:293-360)
+ * and the _kernels.iter_2d_baked / iter_2d_dyn loop (_kernels.py:353-521). */
+typedef struct finom_grid finom_grid;
+int finom_grid_create(int64_t n1, const double *x1_host, int64_t m1, const double *y1_host,
+                      int64_t n2, const double *x2_host, int64_t m2, const double *y2_host,
+                      double eps, void *stream, finom_grid **grid_out);
+int finom_grid_destroy(finom_grid *grid);
+/* info7: n1, m1, n2, m2, table-driven sweeps, square x sweeps, square y sweeps */
+int finom_grid_info(const finom_grid *grid, int64_t *info7);
+/* sinkhorn_2d's loop (run_driver, solver.py:156-199): U_dev (n1 m1), V_dev
+ * (n2 m2) weights; phi_dev / psi_dev out; a_dev / b_dev out: the shift grids
+ * (the loop's work buffers); hist_dev itr_max doubles; info_dev 5 int64 (as
+ * finom_solve1d); absorb_its_dev itr_max int64 (nullable).  The host only
+ * wakes at absorptions (tables rebuilt) and at the end. */
+int finom_solve2d(finom_grid *grid, const double *U_dev, const double *V_dev, double *phi_dev,
+                  double *psi_dev, double *a_dev, double *b_dev, int64_t itr_max, double tol,
+                  int stabilize, double absorb_threshold, double *hist_dev, int64_t *info_dev,
+                  int64_t *absorb_its_dev, void *stream);
+/* transport_cost_fast_2d (kernel2d.py:394-465) of (phi, psi, a, b) into one
+ * device double (a_dev, b_dev both NULL: the plain kernel). */
+int finom_cost2d(finom_grid *grid, const double *phi_dev, const double *psi_dev,
+                 const double *a_dev, const double *b_dev, double *cost_dev, void *stream);
+/* KernelOperator2D.apply / apply_transpose (kernel2d.py:70-90) on device
+ * buffers with shift grids a_dev, b_dev (both NULL: the plain kernel). */
+int finom_apply2d(finom_grid *grid, const double *in_dev, double *out_dev, int transpose,
+                  const double *a_dev, const double *b_dev, void *stream);
+/* The adapter protocol (solver.py:1-16) on a grid: set_shifts = the state
+ * after _GridAdapter.absorb (kernel2d.py:355-360; both NULL: the plain
+ * kernel), iterate2d = _GridAdapter.iterate (kernel2d.py:343-353) in place
+ * with res_dev = (err, status, psmax, psmin, phmax, phmin). */
+int finom_grid_set_shifts(finom_grid *grid, const double *a_dev, const double *b_dev,
+                          void *stream);
+int finom_iterate2d(finom_grid *grid, const double *U_dev, const double *V_dev, double *phi_dev,
+                    double *psi_dev, double *res_dev, void *stream);
 
 /* ---- Row-sharded 2D grids (no reference equivalent) ----
  * One handle per rank for source == target grids x[n] x (y1[m1] | y2[m2]),

@@ -23,6 +23,13 @@ from .solver import (  # noqa: F401
     sinkhorn_1d_batched,
     transport_cost_fast,
 )
-from .kernel2d import KernelOperator2D, build_operator_2d, sinkhorn_2d, transport_cost_fast_2d  # noqa: F401,E501
+from .kernel2d import (  # noqa: F401
+    GpuGridAdapter,
+    GridSolver2D,
+    KernelOperator2D,
+    build_operator_2d,
+    sinkhorn_2d,
+    transport_cost_fast_2d,
+)
 
 __version__ = "0.1.0"

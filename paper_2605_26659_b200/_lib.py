@@ -36,6 +36,7 @@ SIGNATURES = {
     "finom_profile1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_int, _c_dbl,
                                  _vp, _vp, _vp]),
     "finom_solve1d_launches": (_c_i64, [_vp, _c_i64, _c_int]),
+    "finom_solve1d_group": (_c_int, [_vp]),
     "finom_stage_copy": (_c_int, [_c_int, _vp, _vp, _c_i64]),
     "finom_sinkhorn1d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _vp, _vp, _c_dbl, _c_i64,
                                        _c_dbl, _c_int, _c_dbl, _vp, _vp, _vp, _vp, _vp, _vp,
@@ -47,6 +48,17 @@ SIGNATURES = {
                                     _vp, _vp, _vp, _c_int, _vp]),
     "finom_cost2d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl,
                                    _vp, _vp, _vp, _vp, _vp]),
+    "finom_release_memory": (_c_int, []),
+    "finom_grid_create": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _vp,
+                                   _vp]),
+    "finom_grid_destroy": (_c_int, [_vp]),
+    "finom_grid_info": (_c_int, [_vp, _vp]),
+    "finom_solve2d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int, _c_dbl,
+                               _vp, _vp, _vp, _vp]),
+    "finom_cost2d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_apply2d": (_c_int, [_vp, _vp, _vp, _c_int, _vp, _vp, _vp]),
+    "finom_grid_set_shifts": (_c_int, [_vp, _vp, _vp, _vp]),
+    "finom_iterate2d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "finom_grid2d_create": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_i64,
                                      _c_i64, _vp]),
     "finom_grid2d_destroy": (_c_int, [_vp]),
@@ -161,6 +173,46 @@ class Plan1D:
     def close(self):
         if getattr(self, "_h", None):
             self._lib.finom_plan1d_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Grid:
+    """Device plan of a 2D grid pair (finom_grid_create): sweep plans, scratch
+    grids and solve state, reused by every solve / iterate / cost / apply."""
+
+    def __init__(self, x1, y1, x2, y2, eps):
+        lib = load()
+        self._mesh = [np.ascontiguousarray(z, dtype=np.float64) for z in (x1, y1, x2, y2)]
+        x1, y1, x2, y2 = self._mesh
+        self.shape_u = (x1.size, y1.size)
+        self.shape_v = (x2.size, y2.size)
+        self.eps = float(eps)
+        h = ctypes.c_void_p()
+        check(lib.finom_grid_create(x1.size, ptr(x1), y1.size, ptr(y1), x2.size, ptr(x2),
+                                    y2.size, ptr(y2), self.eps, stream_ptr(), ctypes.byref(h)),
+              "finom_grid_create")
+        self._h = h
+        self._lib = lib
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        out = np.zeros(7, dtype=np.int64)
+        check(self._lib.finom_grid_info(self._h, ptr(out)), "finom_grid_info")
+        keys = ("n1", "m1", "n2", "m2", "tables", "square_x", "square_y")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.finom_grid_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -4,7 +4,8 @@
 // (kernel1d.py:142, :148) or np.exp(expo * inv_eps) (_kernels.py:140-159).
 // q_div() reproduces the correctly rounded quotient expo/epsilon with one
 // multiply and two FMAs (checked bit-exact against IEEE division on 2e7
-// random (expo, eps) pairs, see tests/test_fexp_host.py); fexp() is a
+// random (expo, eps) pairs, tests/fexp_check.cu run by
+// tests/test_abi.py::test_fexp_host_arithmetic); fexp() is a
 // 64-entry table + degree-6 polynomial exp, <= 1 ulp from libm, ~12 DP
 // ops instead of ~27 for CUDA's exp() (measured 663 G exp/s on B200 vs
 // 17.9 T DFMA/s, profiles/r01_fp64_probe.txt).  Arguments outside

@@ -2,10 +2,13 @@
 
 The reference builds four table-backed block representations per
 operator (kernel1d.py:194-255) and walks them on one core.  Here an
-operator is only (x, y, eps, a, b): the B200 kernels recompute every
-ratio and edge factor from exactly the same exponent expressions while
-they scan (csrc/finom_1d.cu), so there is nothing to store and nothing to
-rebuild on absorb.  Same public surface: ``dividing_index``,
+operator is only (x, y, eps, a, b): its apply / apply_transpose /
+apply_blocks kernels (csrc/finom_1d.cu k_pre / k_apply) evaluate every ratio
+and edge factor on the fly from exactly the same exponent expressions, so
+an operator stores no tables and absorb only records the shifts.  (The
+solve loop is different: it keeps per-tile tables for the current
+absorption epoch and rebuilds them at every absorption, see DESIGN.md
+section 4.)  Same public surface: ``dividing_index``,
 ``build_operator``, ``apply``, ``apply_transpose``, ``apply_blocks``,
 ``absorb``, ``dense_realization`` (kernel1d.py:55-338).
 """

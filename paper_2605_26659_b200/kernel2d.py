@@ -8,8 +8,7 @@ switches to the dynamic-shift exponent form after the first absorption
 exactly as _GridAdapter does (kernel2d.py:293-360).
 """
 
-import ctypes
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -189,3 +188,127 @@ def transport_cost_fast_2d(solution):
                                      _lib.ptr(phi), _lib.ptr(psi), _lib.ptr(out)),
                "finom_cost2d_host")
     return float(out[0])
+
+
+class GridSolver2D:
+    """Device-resident 2D problem (no reference equivalent; semantics ==
+    sinkhorn_2d): one grid plan (finom_grid_create), weights and iterates in
+    HBM as torch tensors, solve / cost through finom_solve2d / finom_cost2d
+    on the current stream -- the device-pointer form of sinkhorn_2d for
+    callers whose grids already live on the GPU."""
+
+    def __init__(self, source, target, epsilon, u=None, v=None):
+        import torch
+        epsilon = kernel1d._check_eps(epsilon)
+        self.grid = _lib.Grid(source.x_nodes.nodes, source.y_nodes.nodes,
+                              target.x_nodes.nodes, target.y_nodes.nodes, epsilon)
+        (n1, m1), (n2, m2) = self.grid.shape_u, self.grid.shape_v
+        self.N1, self.N2 = n1 * m1, n2 * m2
+        f64 = dict(dtype=torch.float64, device="cuda")
+        self.u = torch.zeros(self.N1, **f64)
+        self.v = torch.zeros(self.N2, **f64)
+        self.phi = torch.empty(self.N1, **f64)
+        self.psi = torch.empty(self.N2, **f64)
+        self.a = torch.empty(self.N1, **f64)
+        self.b = torch.empty(self.N2, **f64)
+        self.cost_dev = torch.zeros(1, **f64)
+        self.info = torch.zeros(5, dtype=torch.int64, device="cuda")
+        self._itr = None
+        if u is not None:
+            self.set_weights(u, v)
+
+    def set_weights(self, u, v):
+        """Weights as flat column-major vectors (numpy or torch)."""
+        import torch
+        for dst, w in ((self.u, u), (self.v, v)):
+            w = getattr(w, "weights", w)
+            if isinstance(w, np.ndarray) and w.ndim == 2:
+                w = w.ravel(order="F")
+            dst.copy_(torch.as_tensor(np.asarray(w) if not torch.is_tensor(w) else w,
+                                      dtype=torch.float64).reshape(-1))
+
+    def solve(self, itr_max, tol=0.0, stabilize=True, absorb_threshold=200.0):
+        """Run sinkhorn_2d's loop on the device buffers; returns the status (0/1/2)."""
+        import torch
+        if self._itr != int(itr_max):
+            self.hist = torch.zeros(int(itr_max), dtype=torch.float64, device="cuda")
+            self.absorb_its = torch.zeros(int(itr_max), dtype=torch.int64, device="cuda")
+            self._itr = int(itr_max)
+        lib = _lib.load()
+        return _lib.check(lib.finom_solve2d(
+            self.grid.handle, _lib.ptr(self.u), _lib.ptr(self.v), _lib.ptr(self.phi),
+            _lib.ptr(self.psi), _lib.ptr(self.a), _lib.ptr(self.b), int(itr_max), float(tol),
+            int(bool(stabilize)), float(absorb_threshold), _lib.ptr(self.hist),
+            _lib.ptr(self.info), _lib.ptr(self.absorb_its), _lib.stream_ptr()), "finom_solve2d")
+
+    def compute_cost(self, absorbed=True):
+        """transport_cost_fast_2d of the current state into cost_dev (device)."""
+        lib = _lib.load()
+        a, b = (self.a, self.b) if absorbed else (None, None)
+        _lib.check(lib.finom_cost2d(self.grid.handle, _lib.ptr(self.phi), _lib.ptr(self.psi),
+                                    _lib.ptr(a), _lib.ptr(b), _lib.ptr(self.cost_dev),
+                                    _lib.stream_ptr()), "finom_cost2d")
+        return self.cost_dev
+
+
+class GpuGridAdapter:
+    """The adapter protocol (solver.py:1-16) on the device grid path: the B200
+    counterpart of _GridAdapter (kernel2d.py:293-360), so run_driver can drive
+    the 2D solve (and A/B-test it against the reference loop).  iterate()
+    runs one finom_iterate2d on the flat vectors in place; absorb() advances
+    the shift grids and rebuilds the sweep tables (finom_grid_set_shifts)."""
+
+    def __init__(self, source, target, epsilon):
+        import torch
+        self.op = build_operator_2d(source, target, epsilon)
+        self.grid = _lib.Grid(source.x_nodes.nodes, source.y_nodes.nodes,
+                              target.x_nodes.nodes, target.y_nodes.nodes, self.op.epsilon)
+        f64 = dict(dtype=torch.float64, device="cuda")
+        (n1, m1), (n2, m2) = source.shape, target.shape
+        self._shape_u, self._shape_v = (n1, m1), (n2, m2)
+        self._U = torch.empty(n1 * m1, **f64)
+        self._V = torch.empty(n2 * m2, **f64)
+        self._PHI = torch.empty(n1 * m1, **f64)
+        self._PSI = torch.empty(n2 * m2, **f64)
+        self._A = None
+        self._B = None
+        self._res = torch.zeros(6, **f64)
+
+    @property
+    def kernel(self):
+        return self.op
+
+    @property
+    def a(self):
+        return self.op.absorption_left.ravel(order="F")
+
+    @property
+    def b(self):
+        return self.op.absorption_right.ravel(order="F")
+
+    def iterate(self, u, v, phi, psi):
+        import torch
+        self._U.copy_(torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)))
+        self._V.copy_(torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)))
+        self._PHI.copy_(torch.from_numpy(np.ascontiguousarray(phi, dtype=np.float64)))
+        self._PSI.copy_(torch.from_numpy(np.ascontiguousarray(psi, dtype=np.float64)))
+        lib = _lib.load()
+        _lib.check(lib.finom_iterate2d(self.grid.handle, _lib.ptr(self._U), _lib.ptr(self._V),
+                                       _lib.ptr(self._PHI), _lib.ptr(self._PSI),
+                                       _lib.ptr(self._res), _lib.stream_ptr()), "finom_iterate2d")
+        phi[:] = self._PHI.cpu().numpy()
+        psi[:] = self._PSI.cpu().numpy()
+        r = self._res.cpu().numpy()
+        return float(r[0]), int(r[1]), float(r[2]), float(r[3]), float(r[4]), float(r[5])
+
+    def absorb(self, delta_a, delta_b):
+        import torch
+        dA = np.asarray(delta_a).reshape(self._shape_u, order="F")
+        dB = np.asarray(delta_b).reshape(self._shape_v, order="F")
+        self.op = absorb_2d(self.op, dA, dB)
+        self._A = torch.from_numpy(np.ascontiguousarray(self.a)).cuda()
+        self._B = torch.from_numpy(np.ascontiguousarray(self.b)).cuda()
+        lib = _lib.load()
+        _lib.check(lib.finom_grid_set_shifts(self.grid.handle, _lib.ptr(self._A),
+                                             _lib.ptr(self._B), _lib.stream_ptr()),
+                   "finom_grid_set_shifts")
