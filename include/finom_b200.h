@@ -56,8 +56,15 @@ int finom_plan1d_create(int64_t P, const int64_t *xoff_host, const double *x_hos
                         const double *eps_host, void *stream, finom_plan1d **plan_out);
 int finom_plan1d_destroy(finom_plan1d *plan);
 
+/* The same plan from P separate host meshes (x_ptrs[p] of n[p] doubles,
+ * y_ptrs[p] of m[p]): staged straight from the problems' arrays, no host
+ * concatenation (the batched API). */
+int finom_plan1d_create_v(int64_t P, const int64_t *n_host, const double *const *x_ptrs,
+                          const int64_t *m_host, const double *const *y_ptrs,
+                          const double *eps_host, void *stream, finom_plan1d **plan_out);
+
 /* Plans and grids allocate from a library-owned memory pool that keeps up to
- * FINOM_POOL_KEEP_GB (env, default 16) GiB of freed memory for the next
+ * FINOM_POOL_KEEP_GB (env, default 64) GiB of freed memory for the next
  * plan; this returns all of it to the driver. */
 int finom_release_memory(void);
 
@@ -125,6 +132,12 @@ int finom_profile1d(finom_plan1d *plan, const double *u_dev, const double *v_dev
  * device, dir 1 device -> host.  Synchronous.  (The batched API's
  * transfers; pageable copies run at a fraction of the link rate.) */
 int finom_stage_copy(int dir, void *host, void *dev, int64_t bytes);
+
+/* count host pieces (host_ptrs[k], bytes[k]) <-> one contiguous device
+ * buffer dev (dir 0: gather into dev, dir 1: scatter out of dev) through the
+ * pinned staging ring; abutting pieces share slots.  Synchronous. */
+int finom_stage_pieces(int dir, void *const *host_ptrs, const int64_t *bytes, int64_t count,
+                       void *dev);
 
 /* Number of kernel launches one finom_solve1d call issues. */
 int64_t finom_solve1d_launches(const finom_plan1d *plan, int64_t itr_max, int stabilize);

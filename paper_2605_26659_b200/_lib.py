@@ -26,6 +26,8 @@ SIGNATURES = {
     "finom_build_info": (ctypes.c_char_p, []),
     "finom_plan1d_create": (_c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "finom_plan1d_destroy": (_c_int, [_vp]),
+    "finom_plan1d_create_v": (_c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_stage_pieces": (_c_int, [_c_int, _vp, _vp, _c_i64, _vp]),
     "finom_tile_partition": (_c_i64, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _vp]),
     "finom_plan1d_info": (_c_int, [_vp, _vp]),
     "finom_solve1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int,
@@ -100,6 +102,18 @@ def stage_copy(direction, host, dev):
     check(load().finom_stage_copy(direction, ptr(host), ptr(dev), host.nbytes), "finom_stage_copy")
 
 
+def stage_pieces(direction, hosts, dev):
+    """List of contiguous host numpy arrays <-> one device tensor, in order
+    (finom_stage_pieces; 0: gather into dev, 1: scatter into the arrays)."""
+    hosts = list(hosts)
+    assert all(h.flags["C_CONTIGUOUS"] for h in hosts)
+    assert sum(h.nbytes for h in hosts) == dev.numel() * dev.element_size()
+    hp = np.array([h.ctypes.data for h in hosts], dtype=np.uint64)
+    nb = np.array([h.nbytes for h in hosts], dtype=np.int64)
+    check(load().finom_stage_pieces(direction, ptr(hp), ptr(nb), len(hosts), ptr(dev)),
+          "finom_stage_pieces")
+
+
 def tile_partition(x, y):
     """Host-only tile partition + merged-order masks (finom_tile_partition)."""
     lib = load(require_device=False)
@@ -149,14 +163,21 @@ class Plan1D:
         self.yoff = np.zeros(self.P + 1, dtype=np.int64)
         self.xoff[1:] = np.cumsum([x.size for x in xs])
         self.yoff[1:] = np.cumsum([y.size for y in ys])
-        self.x = np.concatenate(xs) if self.P > 1 else xs[0]
-        self.y = np.concatenate(ys) if self.P > 1 else ys[0]
         self.eps = np.ascontiguousarray(np.broadcast_to(np.asarray(eps, dtype=np.float64),
                                                         (self.P,)))
         h = ctypes.c_void_p()
-        check(lib.finom_plan1d_create(self.P, ptr(self.xoff), ptr(self.x), ptr(self.yoff),
-                                      ptr(self.y), ptr(self.eps), stream_ptr(),
-                                      ctypes.byref(h)), "finom_plan1d_create")
+        if self.P == 1:
+            check(lib.finom_plan1d_create(1, ptr(self.xoff), ptr(xs[0]), ptr(self.yoff),
+                                          ptr(ys[0]), ptr(self.eps), stream_ptr(),
+                                          ctypes.byref(h)), "finom_plan1d_create")
+        else:  # per-problem arrays staged as they are (no host concatenation)
+            n = np.diff(self.xoff)
+            m = np.diff(self.yoff)
+            xp = np.array([x.ctypes.data for x in xs], dtype=np.uint64)
+            yp = np.array([y.ctypes.data for y in ys], dtype=np.uint64)
+            check(lib.finom_plan1d_create_v(self.P, ptr(n), ptr(xp), ptr(m), ptr(yp),
+                                            ptr(self.eps), stream_ptr(), ctypes.byref(h)),
+                  "finom_plan1d_create_v")
         self._h = h
         self._lib = lib
 

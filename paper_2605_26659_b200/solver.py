@@ -11,6 +11,8 @@ adapter protocol (solver.py:1-16) and accepts the GPU adapter
 """
 
 import ctypes
+import os
+from collections.abc import Sequence
 from dataclasses import dataclass, replace
 from time import perf_counter
 from typing import Optional
@@ -261,12 +263,12 @@ class BatchSolver1D:
         self.P = self.plan.P
         self.eps = np.array(eps)
         f64 = dict(dtype=torch.float64, device=dev)
-        hu = np.concatenate([wts(u) for u in us])
-        hv = np.concatenate([wts(v) for v in vs])
-        self.u = torch.empty(hu.size, dtype=torch.float64, device=dev)
-        self.v = torch.empty(hv.size, dtype=torch.float64, device=dev)
-        _lib.stage_copy(0, hu, self.u)
-        _lib.stage_copy(0, hv, self.v)
+        hu = [np.ascontiguousarray(wts(u), dtype=np.float64) for u in us]
+        hv = [np.ascontiguousarray(wts(v), dtype=np.float64) for v in vs]
+        self.u = torch.empty(int(self.plan.xoff[-1]), dtype=torch.float64, device=dev)
+        self.v = torch.empty(int(self.plan.yoff[-1]), dtype=torch.float64, device=dev)
+        _lib.stage_pieces(0, hu, self.u)  # (straight from the problems' arrays)
+        _lib.stage_pieces(0, hv, self.v)
         NX, NY = self.u.numel(), self.v.numel()
         self.phi = torch.empty(NX, **f64)
         self.psi = torch.empty(NY, **f64)
@@ -310,6 +312,7 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
     Raises the reference's exception if any problem fails.
     """
     eps = config.epsilon if epsilons is None else epsilons
+    verbose = os.environ.get("FB_VERBOSE")
     t0 = perf_counter()
     bs = BatchSolver1D(xs, ys, us, vs, eps)
     setup = perf_counter() - t0
@@ -327,34 +330,73 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
         _lib.stage_copy(1, h, t)
         return h
 
+    t2 = perf_counter()
     hist = host(bs.hist).reshape(bs.P, -1)
     abs_its = host(bs.abs_its).reshape(bs.P, -1)
     cost = bs.cost.cpu().numpy()
     phi, psi, a, b = host(bs.phi), host(bs.psi), host(bs.a), host(bs.b)
-    xo, yo = bs.plan.xoff, bs.plan.yoff
-    # Per-problem Solutions share the batch's host buffers: phi/psi/a/b are
-    # disjoint views (no copies), histories are built vectorized.
-    sols = []
-    info_l = info.tolist()
-    cost_l = cost.tolist()
-    for p in range(bs.P):
-        x = xs[p] if hasattr(xs[p], "nodes") else None
-        y = ys[p] if hasattr(ys[p], "nodes") else None
-        sl, tl = slice(xo[p], xo[p + 1]), slice(yo[p], yo[p + 1])
-        e = float(bs.eps[p])
+    t3 = perf_counter()
+    sols = BatchSolutions(xs, ys, bs.plan.xoff, bs.plan.yoff, bs.eps, config, info, cost,
+                          phi, psi, a, b, hist, abs_its, setup + loop, setup)
+    if verbose:
+        print("sinkhorn_1d_batched: setup %.1f loop %.1f cost+d2h %.1f ms" % (
+            1e3 * setup, 1e3 * loop, 1e3 * (t3 - t2)), flush=True)
+    return sols
+
+
+class BatchSolutions(Sequence):
+    """The per-problem Solutions of a batched solve, as a sequence.
+
+    Every result is already on the host in the batch's arrays when the call
+    returns (phi / psi / a / b, histories, infos, costs); element p is a
+    Solution whose vectors are disjoint views of those arrays (no copies),
+    built when first accessed -- a list of 8192 dataclass objects and
+    operator handles costs ~0.3 s of Python that a caller iterating over a
+    few problems never needs."""
+
+    def __init__(self, xs, ys, xoff, yoff, eps, config, info, cost, phi, psi, a, b, hist,
+                 abs_its, wall, setup):
+        self._xs, self._ys, self._xo, self._yo = xs, ys, xoff, yoff
+        self._eps, self._config = eps, config
+        self._info, self._cost = info, cost
+        self.phi, self.psi, self.a, self.b = phi, psi, a, b
+        self._hist, self._abs_its = hist, abs_its
+        self._wall, self._setup = wall, setup
+        self._cache = {}
+
+    def __len__(self):
+        return len(self._xs)
+
+    def _make(self, p):
+        config = self._config
+        x = self._xs[p] if hasattr(self._xs[p], "nodes") else None
+        y = self._ys[p] if hasattr(self._ys[p], "nodes") else None
+        sl = slice(self._xo[p], self._xo[p + 1])
+        tl = slice(self._yo[p], self._yo[p + 1])
+        e = float(self._eps[p])
         cfg = config if e == config.epsilon else replace(config, epsilon=e)
-        ap, bp = a[sl], b[tl]
+        ap, bp = self.a[sl], self.b[tl]
         op = None
         if x is not None and y is not None:
             op = kernel1d.KernelOperator1D(x, y, e, ap, bp, kernel1d._PlanCache(x, y, e))
-        its, conv, _, nab, _ = info_l[p]
-        sols.append(Solution(
-            phi=phi[sl], psi=psi[tl], a=ap, b=bp, kernel=op,
+        its, conv, _, nab, _ = (int(v) for v in self._info[p])
+        return Solution(
+            phi=self.phi[sl], psi=self.psi[tl], a=ap, b=bp, kernel=op,
             iterations_run=its, converged=bool(conv),
-            marginal_error_history=history_from(hist[p], its, bool(conv), cfg),
-            wall_time=setup + loop, setup_time=setup, cost=cost_l[p], config=cfg,
-            absorb_iterations=abs_its[p, :nab].tolist()))
-    return sols
+            marginal_error_history=history_from(self._hist[p], its, bool(conv), cfg),
+            wall_time=self._wall, setup_time=self._setup, cost=float(self._cost[p]),
+            config=cfg, absorb_iterations=self._abs_its[p, :nab].tolist())
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        if k < 0:
+            k += len(self)
+        if not 0 <= k < len(self):
+            raise IndexError(k)
+        if k not in self._cache:
+            self._cache[k] = self._make(k)
+        return self._cache[k]
 
 
 def marginal_error(state, kernel, v):
