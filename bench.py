@@ -164,23 +164,66 @@ def run_2d(args, cfg, wl, world=1, rank=0):
         run = lambda: S.sinkhorn_2d_row_sharded(src, tgt, mu, mv, scfg)
     else:
         run = lambda: fb.sinkhorn_2d(src, tgt, mu, mv, scfg)
-    for _ in range(max(1, min(args.warmup, 2))):
+    launches = None
+    if world > 1:
+        for _ in range(max(1, min(args.warmup, 2))):
+            run()
+        loops, walls = [], []
+        clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+        clocks.start()
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            sol = run()
+            walls.append(time.perf_counter() - t0)
+            loops.append(sol.wall_time - sol.setup_time)
+        ck = clocks.stop()
+        loop = statistics.median(loops)
+    else:
+        # device-resident solve (GridSolver2D: weights and iterates in HBM,
+        # finom_solve2d), CUDA events on its stream around the K timed solves
+        import torch
+        gs = fb.GridSolver2D(src, tgt, wl["eps"][0], mu, mv)
+        for _ in range(max(args.warmup, 3)):
+            gs.solve(wl["itr"], 0.0, True, 200.0)
+        torch.cuda.synchronize()
+        clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+        clocks.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            gs.solve(wl["itr"], 0.0, True, 200.0)
+        e1.record()
+        torch.cuda.synchronize()
+        ck = clocks.stop()
+        loop = e0.elapsed_time(e1) * 1e-3 / args.steps
+        loops = [loop]
+        launches = gs.grid.info()["launches"] * args.steps
+        del gs
+        # end to end: the public host-array API (plan, copies, loop, cost, results out)
         run()
-    loops, walls = [], []
-    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
-    clocks.start()
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        sol = run()
-        walls.append(time.perf_counter() - t0)
-        loops.append(sol.wall_time - sol.setup_time)
-    ck = clocks.stop()
-    loop = statistics.median(loops)
+        walls = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            sol = run()
+            walls.append(time.perf_counter() - t0)
     if rank != 0:
         return
     # roofline of the whole iteration: 88 B/pt before the first
     # absorption, 120 B/pt after (the two-sweep algorithm with a materialised
     # intermediate), weighted by the iterations spent in either state
+    cpu = None
+    if not args.no_cpu_baseline:
+        # the C port (oracle/) of the reference's 2D loop on one host core: a
+        # bounded number of iterations of the full-size grid, wall clock of the
+        # call (its setup is O(n + m) table builds, negligible at these sizes)
+        from oracle import oracle as O
+        its = 60 if cfg == 3 else 3
+        t0 = time.perf_counter()
+        O.sinkhorn_2d(x1, y1, x2, y2, U, V, wl["eps"][0], its, 0.0, True)
+        dt = time.perf_counter() - t0
+        cpu = {"value": pts * its / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": "config%d full-size grid, first %d of %d iterations (stabilize=True), "
+                         "wall clock of the call" % (cfg, its, wl["itr"])}
     a0 = sol.absorb_iterations[0] if len(sol.absorb_iterations) else sol.iterations_run
     abytes = pts * (88.0 * a0 + 120.0 * (sol.iterations_run - a0))
     peak, psrc = peaks()
@@ -194,9 +237,10 @@ def run_2d(args, cfg, wl, world=1, rank=0):
         "config": {"workload": "config%d: 2D %dx%d eps=%g %d it (stabilize=True)" % (
             cfg, x1.size, y1.size, wl["eps"][0], wl["itr"]), "itr_max": wl["itr"],
             "parallelism": "row shards x%d (carry exchange)" % world if world > 1 else "1 GPU",
-            "timing": "loop window (max over ranks); " + (
-                "host-driven loop, one sync per iteration" if world > 1 else
-                "device-looped CUDA graph, host sync only at absorptions")},
+            "timing": ("loop window (max over ranks); host-driven loop, one sync per "
+                       "iteration") if world > 1 else (
+                "CUDA events around K device-resident solves (GridSolver2D / finom_solve2d: "
+                "device-looped CUDA graph, host sync only at absorptions)")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": psrc,
                      "kernel": "whole iteration: 4 line sweeps (k_sq_pre/k_sq_scan/k_sq_apply) "
@@ -206,6 +250,8 @@ def run_2d(args, cfg, wl, world=1, rank=0):
         "e2e": {"value": pts * wl["itr"] / statistics.median(walls), "unit": UNIT,
                 "h2d_bytes_per_step": 8 * (2 * pts + 2 * x1.size + 2 * y1.size),
                 "d2h_bytes_per_step": 8 * 4 * pts},
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
         "iterations_run": sol.iterations_run, "absorbs": sol.absorb_iterations,
         "cost": sol.cost, "clocks": ck, "loops_ms": [round(1e3 * x, 2) for x in loops],
     }

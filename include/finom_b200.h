@@ -197,8 +197,9 @@ int finom_grid_create(int64_t n1, const double *x1_host, int64_t m1, const doubl
                       int64_t n2, const double *x2_host, int64_t m2, const double *y2_host,
                       double eps, void *stream, finom_grid **grid_out);
 int finom_grid_destroy(finom_grid *grid);
-/* info7: n1, m1, n2, m2, table-driven sweeps, square x sweeps, square y sweeps */
-int finom_grid_info(const finom_grid *grid, int64_t *info7);
+/* info8: n1, m1, n2, m2, table-driven sweeps, square x sweeps, square y
+ * sweeps, kernel launches of the last finom_solve2d (graph nodes counted) */
+int finom_grid_info(const finom_grid *grid, int64_t *info8);
 /* sinkhorn_2d's loop (run_driver, solver.py:156-199): U_dev (n1 m1), V_dev
  * (n2 m2) weights; phi_dev / psi_dev out; a_dev / b_dev out: the shift grids
  * (the loop's work buffers); hist_dev itr_max doubles; info_dev 5 int64 (as

@@ -226,9 +226,9 @@ class Grid:
         return self._h
 
     def info(self):
-        out = np.zeros(7, dtype=np.int64)
+        out = np.zeros(8, dtype=np.int64)
         check(self._lib.finom_grid_info(self._h, ptr(out)), "finom_grid_info")
-        keys = ("n1", "m1", "n2", "m2", "tables", "square_x", "square_y")
+        keys = ("n1", "m1", "n2", "m2", "tables", "square_x", "square_y", "launches")
         return dict(zip(keys, (int(v) for v in out)))
 
     def close(self):
