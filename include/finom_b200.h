@@ -226,6 +226,22 @@ int finom_grid_set_shifts(finom_grid *grid, const double *a_dev, const double *b
 int finom_iterate2d(finom_grid *grid, const double *U_dev, const double *V_dev, double *phi_dev,
                     double *psi_dev, double *res_dev, void *stream);
 
+/* ---- Dense realizations / plans on the device (small sizes) ----
+ * finom_dense1d: out (n x m, row-major) = kernel1d.dense_realization
+ * (kernel1d.py:328-338), exp(((-|x_i - y_j| + a_i) + b_j) / eps) with
+ * a_dev / b_dev nullable (zero); with phi_dev / psi_dev (both or neither) the
+ * transport plan of solver.plan_dense (solver.py:240-249),
+ * (phi_i * K'_ij) * psi_j.  finom_dense2d: the same for grids
+ * (kernel2d.dense_realization_2d, kernel2d.py:278-290), (n1 m1) x (n2 m2)
+ * over the flat column-major grid vectors. */
+int finom_dense1d(int64_t n, int64_t m, const double *x_dev, const double *y_dev,
+                  const double *a_dev, const double *b_dev, double eps, const double *phi_dev,
+                  const double *psi_dev, double *out_dev, void *stream);
+int finom_dense2d(int64_t n1, int64_t m1, int64_t n2, int64_t m2, const double *x1_dev,
+                  const double *y1_dev, const double *x2_dev, const double *y2_dev,
+                  const double *a_dev, const double *b_dev, double eps, const double *phi_dev,
+                  const double *psi_dev, double *out_dev, void *stream);
+
 /* ---- Row-sharded 2D grids (no reference equivalent) ----
  * One handle per rank for source == target grids x[n] x (y1[m1] | y2[m2]),
  * rank holding grid rows [k0, k1).  The caller drives run_driver's loop

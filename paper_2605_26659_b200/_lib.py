@@ -51,6 +51,9 @@ SIGNATURES = {
     "finom_cost2d_host": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl,
                                    _vp, _vp, _vp, _vp, _vp]),
     "finom_release_memory": (_c_int, []),
+    "finom_dense1d": (_c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _c_dbl, _vp, _vp, _vp, _vp]),
+    "finom_dense2d": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _c_dbl, _vp, _vp, _vp, _vp]),
     "finom_grid_create": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _vp,
                                    _vp]),
     "finom_grid_destroy": (_c_int, [_vp]),
@@ -241,3 +244,34 @@ class Grid:
             self.close()
         except Exception:
             pass
+
+
+def _dev(a):
+    import torch
+    return None if a is None else torch.from_numpy(
+        np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def dense1d(x, y, a, b, eps, phi=None, psi=None):
+    """Dense kernel (or plan with phi / psi) of a 1D pair on the device
+    (finom_dense1d); returns a host n x m array."""
+    import torch
+    n, m = len(x), len(y)
+    args = [_dev(z) for z in (x, y, a, b, phi, psi)]
+    out = torch.empty(n * m, dtype=torch.float64, device="cuda")
+    check(load().finom_dense1d(n, m, *(ptr(z) for z in args[:4]), float(eps),
+                               ptr(args[4]), ptr(args[5]), ptr(out), stream_ptr()),
+          "finom_dense1d")
+    return out.cpu().numpy().reshape(n, m)
+
+
+def dense2d(x1, y1, x2, y2, A, B, eps, phi=None, psi=None):
+    """Dense kernel (or plan) of a grid pair on the device (finom_dense2d)."""
+    import torch
+    n1, m1, n2, m2 = len(x1), len(y1), len(x2), len(y2)
+    args = [_dev(z) for z in (x1, y1, x2, y2, A, B, phi, psi)]
+    out = torch.empty(n1 * m1 * n2 * m2, dtype=torch.float64, device="cuda")
+    check(load().finom_dense2d(n1, m1, n2, m2, *(ptr(z) for z in args[:6]), float(eps),
+                               ptr(args[6]), ptr(args[7]), ptr(out), stream_ptr()),
+          "finom_dense2d")
+    return out.cpu().numpy().reshape(n1 * m1, n2 * m2)

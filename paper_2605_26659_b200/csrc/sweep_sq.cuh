@@ -17,8 +17,10 @@
 //   delta_r = exp((alpha_r + beta_r) / eps)                  diagonal edge
 //   sigma_r = exp((-g_{r+1} + alpha_r - alpha_{r+1}) / eps)  upper ratio
 //   mu_r    = exp((-g_{r+1} + alpha_r + beta_{r+1}) / eps)   upper edge
-// -- the reference's exponent expressions (kernel1d.py:121-159, dyn form
-// _kernels.py:128-203), evaluated once per absorption epoch.
+// -- the reference's exponent expressions: "/ eps" (kernel1d.py:121-159)
+// for the baked tables before the first absorption, "* inv_eps"
+// (_kernels.py:128-203) for the dyn form after it; evaluated once per
+// absorption epoch.
 //
 // Records per tile of SQT = 256 points (lane l holds points 8l .. 8l+7):
 //   F: (rho, delta) then (sigma, mu), double2 at [j][k][lane]   (8 KB)
@@ -84,6 +86,9 @@ struct SqArgs {
   int n, lines, tl;       // points per line, lines, tiles per line
   int shared;             // records shared by every line (no shifts)
   double inv;             // 1 / eps
+  double eps;
+  int baked;              // k_sq_build: the baked (pre-absorption) exponents x / eps
+                          // (kernel1d.py:142, :148) instead of the dyn x * inv_eps
   // fused scaling update (nullable ew: plain sweep): SC <- W / out over the
   // flat grid out_t addresses, marginal error (eerr), extremes, failures;
   // per-CTA partials into epart (k_epi_fold reduces them in a fixed order)
@@ -111,19 +116,23 @@ __global__ void __launch_bounds__(NTHR) k_sq_build(SqArgs a) {
   auto A = [&](int r) { return al ? al[r] : 0.0; };
   auto B = [&](int r) { return be ? be[r] : 0.0; };
   const int r0 = t * SQT + EPT * lane;
+  // exponent argument: baked tables divide by eps (kernel1d.py:142, :148;
+  // q_div is the IEEE quotient), the dyn form multiplies by inv_eps
+  // (_kernels.py:140-159)
+  auto arg = [&](double num) { return a.baked ? q_div(num, a.eps, a.inv) : __dmul_rn(num, a.inv); };
   double rho[EPT], del[EPT], sig[EPT], mu[EPT];
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int r = r0 + k;
     rho[k] = 1.0; del[k] = 0.0; sig[k] = 1.0; mu[k] = 0.0;  // padding: identity steps
     if (r < a.n) {
-      del[k] = exp(__dmul_rn(__dadd_rn(A(r), B(r)), a.inv));
+      del[k] = exp(arg(__dadd_rn(A(r), B(r))));
       if (r > 0 || a.k0 > 0)  // (a window's first point: the mesh point before it is a.Z[-1])
-        rho[k] = exp(__dmul_rn(__dadd_rn(-(a.Z[r] - a.Z[r - 1]), __dsub_rn(A(r), A(r - 1))), a.inv));
+        rho[k] = exp(arg(__dadd_rn(-(a.Z[r] - a.Z[r - 1]), __dsub_rn(A(r), A(r - 1)))));
       if (r + 1 < a.n) {
         const double g = a.Z[r + 1] - a.Z[r];
-        sig[k] = exp(__dmul_rn(__dadd_rn(-g, __dsub_rn(A(r), A(r + 1))), a.inv));
-        mu[k] = exp(__dmul_rn(__dadd_rn(-g, __dadd_rn(A(r), B(r + 1))), a.inv));
+        sig[k] = exp(arg(__dadd_rn(-g, __dsub_rn(A(r), A(r + 1)))));
+        mu[k] = exp(arg(__dadd_rn(-g, __dadd_rn(A(r), B(r + 1)))));
       }
     }
   }
@@ -298,8 +307,11 @@ __global__ void k_sq_seg_tot(SqArgs a, double *out) {
     if (a.k0 > 0) {
       const double g = a.Z[0] - a.Z[-1];
       const double be = a.beta ? a.beta[(size_t)p * a.n] : 0.0;
-      const double sig = exp(__dmul_rn(__dadd_rn(-g, __dsub_rn(0.0, 0.0)), a.inv));
-      const double mu = exp(__dmul_rn(__dadd_rn(-g, __dadd_rn(0.0, be)), a.inv));
+      auto arg = [&](double num) {
+        return a.baked ? q_div(num, a.eps, a.inv) : __dmul_rn(num, a.inv);
+      };
+      const double sig = exp(arg(__dadd_rn(-g, __dsub_rn(0.0, 0.0))));
+      const double mu = exp(arg(__dadd_rn(-g, __dadd_rn(0.0, be))));
       const double v0 = a.vin[(size_t)p * a.n];
       A = gm(sig, A);
       C = __dadd_rn(gm(sig, C), __dmul_rn(mu, v0));

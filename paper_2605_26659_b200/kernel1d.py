@@ -177,9 +177,7 @@ def absorb(op, delta_a, delta_b):
 
 
 def dense_realization(op):
-    """Dense matrix, entry by entry (tests / small-scale debugging; kernel1d.py:328-338)."""
-    x = op.x_mesh.nodes
-    y = op.y_mesh.nodes
-    expo = -np.abs(np.subtract.outer(x, y))
-    expo = expo + op.absorption_left[:, None] + op.absorption_right[None, :]
-    return np.exp(expo / op.epsilon)
+    """Dense matrix, entry by entry on the device (tests / small-scale debugging;
+    kernel1d.py:328-338: exp(((-|x_i - y_j| + a_i) + b_j) / eps), finom_dense1d)."""
+    return _lib.dense1d(op.x_mesh.nodes, op.y_mesh.nodes, op.absorption_left,
+                        op.absorption_right, op.epsilon)

@@ -114,14 +114,16 @@ def absorb_2d(op, delta_a, delta_b):
                             op.absorption_right + delta_b)
 
 
-def dense_realization_2d(op):
-    """Vectorized dense matrix, for tests and small instances (kernel2d.py:278-290)."""
-    full = np.kron(op.ky.dense_realization(), op.kx.dense_realization())
+def dense_realization_2d(op, phi=None, psi=None):
+    """Vectorized dense matrix on the device, for tests and small instances
+    (kernel2d.py:278-290: kron(Ky, Kx) [* exp((A_I + B_J) / eps)],
+    finom_dense2d); with phi / psi the plan diag(phi) K diag(psi)."""
+    x1, y1, x2, y2 = op._meshes()
+    A = B = None
     if op.absorbed:
-        av = op.absorption_left.ravel(order="F")
-        bv = op.absorption_right.ravel(order="F")
-        full = full * np.exp((av[:, None] + bv[None, :]) / op.epsilon)
-    return full
+        A = op.absorption_left.ravel(order="F")
+        B = op.absorption_right.ravel(order="F")
+    return _lib.dense2d(x1, y1, x2, y2, A, B, op.epsilon, phi, psi)
 
 
 def sinkhorn_2d(source, target, u, v, config):

@@ -407,13 +407,17 @@ def marginal_error(state, kernel, v):
 
 
 def plan_dense(solution):
-    """diag(phi) K diag(psi) (solver.py:240-249)."""
+    """diag(phi) K diag(psi) (solver.py:240-249), materialized on the device
+    in one pass: (phi_i * K'_ij) * psi_j (finom_dense1d / finom_dense2d)."""
     kern = solution.kernel
     n, m = kern.shape
     if n * m > solution.config.plan_cap:
         raise SizeCapExceeded("plan has %d entries, cap is %d" % (n * m, solution.config.plan_cap))
-    dense = kern.dense_realization()
-    return solution.phi[:, None] * dense * solution.psi[None, :]
+    if isinstance(kern, kernel1d.KernelOperator1D):
+        return _lib.dense1d(kern.x_mesh.nodes, kern.y_mesh.nodes, kern.absorption_left,
+                            kern.absorption_right, kern.epsilon, solution.phi, solution.psi)
+    from .kernel2d import dense_realization_2d
+    return dense_realization_2d(kern, solution.phi, solution.psi)
 
 
 def transport_cost_fast(solution):

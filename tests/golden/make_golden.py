@@ -339,3 +339,40 @@ def config4_full():
 
 if __name__ == "__main__" and "config4_full" in sys.argv[1:]:
     config4_full()
+
+
+def dense_cases():
+    """SURVEY 8(f) f1 pins: the reference's dense_realization (1D, 2D; plain and
+    shifted), plan_dense and marginal_error of solved states."""
+    out = {}
+    rng = np.random.default_rng(91)
+    # 1D: a solved, absorbed problem (the Solution's kernel carries shifts)
+    x, y, u, v, eps = W.config1(n=300)
+    cfg = rs.SolverConfig(epsilon=eps, itr_max=40, tol=0.0, stabilize=True, absorb_threshold=6.0)
+    X, Y, Um, Vm = rm.Mesh1D(x), rm.Mesh1D(y), rm.Measure(u), rm.Measure(v)
+    sol = rs.sinkhorn_1d(X, Y, Um, Vm, cfg)
+    out.update(s1_x=x, s1_y=y, s1_u=u, s1_v=v, s1_eps=np.array(eps),
+               s1_phi=sol.phi, s1_psi=sol.psi, s1_a=np.asarray(sol.a), s1_b=np.asarray(sol.b),
+               s1_dense=rk.dense_realization(sol.kernel), s1_plan=rs.plan_dense(sol),
+               s1_marg=np.array(rs.marginal_error(sol, sol.kernel, Vm)))
+    # 1D: random operator with shifts, arbitrary state
+    n, m = 37, 53
+    x2 = np.sort(rng.uniform(0, 1, n)); y2 = np.sort(rng.uniform(0, 1, m))
+    a2 = rng.normal(0, 0.02, n); b2 = rng.normal(0, 0.02, m)
+    op = rk.absorb(rk.build_operator(rm.Mesh1D(x2), rm.Mesh1D(y2), 0.05), a2, b2)
+    out.update(r1_x=x2, r1_y=y2, r1_a=a2, r1_b=b2, r1_eps=np.array(0.05),
+               r1_dense=rk.dense_realization(op))
+    # 2D: grid operator, plain and absorbed
+    x1, y1, xg, yg = (np.sort(rng.uniform(0, 1, k)) for k in (6, 5, 4, 7))
+    src = rm.Grid2D(rm.Mesh1D(x1), rm.Mesh1D(y1))
+    tgt = rm.Grid2D(rm.Mesh1D(xg), rm.Mesh1D(yg))
+    op2 = r2.build_operator_2d(src, tgt, 0.1)
+    A = rng.normal(0, 0.05, (6, 5)); B = rng.normal(0, 0.05, (4, 7))
+    op2a = r2.absorb_2d(op2, A, B)
+    out.update(g_x1=x1, g_y1=y1, g_x2=xg, g_y2=yg, g_A=A, g_B=B, g_eps=np.array(0.1),
+               g_dense=r2.dense_realization_2d(op2), g_dense_abs=r2.dense_realization_2d(op2a))
+    save("dense_cases.npz", **out)
+
+
+if __name__ == "__main__" and "dense" in sys.argv[1:]:
+    dense_cases()

@@ -73,10 +73,12 @@ def test_config3_full_vs_reference_pins():
     from test_parity_gpu import hist_ok
     q = dict(hist=hist_ok([h[1] for h in sol.marginal_error_history], g["hist_err"]),
              phi=rel_inf(sol.phi[::st], g["phi_s"]), psi=rel_inf(sol.psi[::st], g["psi_s"]),
+             a=rel_inf(sol.a[::st], g["a_s"]), b=rel_inf(sol.b[::st], g["b_s"]),
              cost=abs(sol.cost - float(g["cost"])) / abs(float(g["cost"])))
     print("config3 full parity", q)
     assert list(sol.absorb_iterations) == [int(t) for t in g["absorb_its"]]
     assert q["hist"] < 1 and q["phi"] < TOL and q["psi"] < TOL and q["cost"] < TOL, q
+    assert q["a"] < TOL and q["b"] < TOL, q
 
 
 @pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "config4_full_pins.npz")),
@@ -97,6 +99,7 @@ def test_config4_full_vs_reference_pins():
     print("config4 full parity", q)
     assert list(sol.absorb_iterations) == [int(t) for t in g["absorb_its"]]
     assert q["hist"] < 1 and q["phi"] < TOL and q["psi"] < TOL and q["cost"] < TOL, q
+    assert q["a"] < TOL and q["b"] < TOL, q
 
 
 def _sharded_case(n, m1, m2, eps, itr, seed, zero_rows=False, thr=200.0, square_y=False):
