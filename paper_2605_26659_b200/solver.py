@@ -416,8 +416,11 @@ def plan_dense(solution):
     if isinstance(kern, kernel1d.KernelOperator1D):
         return _lib.dense1d(kern.x_mesh.nodes, kern.y_mesh.nodes, kern.absorption_left,
                             kern.absorption_right, kern.epsilon, solution.phi, solution.psi)
-    from .kernel2d import dense_realization_2d
-    return dense_realization_2d(kern, solution.phi, solution.psi)
+    from .kernel2d import KernelOperator2D, dense_realization_2d
+    if isinstance(kern, KernelOperator2D):
+        return dense_realization_2d(kern, solution.phi, solution.psi)
+    dense = kern.dense_realization()  # (the dense baseline's kernel)
+    return solution.phi[:, None] * dense * solution.psi[None, :]
 
 
 def transport_cost_fast(solution):
