@@ -242,6 +242,38 @@ int finom_dense2d(int64_t n1, int64_t m1, int64_t n2, int64_t m2, const double *
                   const double *a_dev, const double *b_dev, double eps, const double *phi_dev,
                   const double *psi_dev, double *out_dev, void *stream);
 
+/* ---- Distributed 1D scan (BASELINE north star; no reference equivalent) ----
+ * One 1D problem split into R segments of the merged order x U y (merge-path
+ * splits at diagonals r (n+m) / R, ties never split), one per rank.  The
+ * caller drives run_driver and the collectives
+ * (paper_2605_26659_b200.sharding.sinkhorn_1d_segmented): per half,
+ * finom_seg1d_pre writes the segment's totals of both recurrences
+ * (_kernels.py:53-88; 10 doubles), the caller all-gathers them ([R][10]),
+ * finom_seg1d_finish composes the other segments' totals into the segment's
+ * incoming states, computes its rows and their scaling update, and writes
+ * its partials (err, max, min, status or -1) for a rank-order combine.
+ * Data arrays (weights, scalings, shifts) are whole-length on every rank.
+ * half 0 = psi <- v / K'^T phi, half 1 = phi <- u / K' psi. */
+typedef struct finom_seg1d finom_seg1d;
+/* bounds: 2 (R + 1) int64, the split points (i_k, j_k), k = 0..R (host only) */
+int finom_seg1d_split(int64_t n, const double *x, int64_t m, const double *y, int64_t R,
+                      int64_t *bounds);
+int finom_seg1d_create(int64_t n, const double *x_host, int64_t m, const double *y_host,
+                       double eps, int64_t R, int64_t r, void *stream, finom_seg1d **out);
+int finom_seg1d_destroy(finom_seg1d *seg);
+/* w4: the segment's windows x [w0, w1), y [w2, w3) */
+int finom_seg1d_window(const finom_seg1d *seg, int64_t *w4);
+int finom_seg1d_pre(finom_seg1d *seg, int half, const double *in_dev, const double *a_dev,
+                    const double *b_dev, double *tot_out_dev, void *stream);
+int finom_seg1d_finish(finom_seg1d *seg, int half, const double *in_dev, const double *a_dev,
+                       const double *b_dev, const double *tot_all_dev, const double *W_dev,
+                       double *SC_dev, double *part_out_dev, void *stream);
+/* shift += _shift(W, SC) (solver.py:135-153) over the whole vector; SC all
+ * scalings, prv / nxt the previous / next positive-mass index of W */
+int finom_seg1d_absorb(finom_seg1d *seg, int side, double *shift_dev, const double *W_dev,
+                       const double *SC_dev, const int32_t *prv_dev, const int32_t *nxt_dev,
+                       void *stream);
+
 /* ---- Row-sharded 2D grids (no reference equivalent) ----
  * One handle per rank for source == target grids x[n] x (y1[m1] | y2[m2]),
  * rank holding grid rows [k0, k1).  The caller drives run_driver's loop

@@ -64,6 +64,13 @@ SIGNATURES = {
     "finom_apply2d": (_c_int, [_vp, _vp, _vp, _c_int, _vp, _vp, _vp]),
     "finom_grid_set_shifts": (_c_int, [_vp, _vp, _vp, _vp]),
     "finom_iterate2d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_seg1d_split": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp]),
+    "finom_seg1d_create": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_dbl, _c_i64, _c_i64, _vp, _vp]),
+    "finom_seg1d_destroy": (_c_int, [_vp]),
+    "finom_seg1d_window": (_c_int, [_vp, _vp]),
+    "finom_seg1d_pre": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "finom_seg1d_finish": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_seg1d_absorb": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "finom_grid2d_create": (_c_int, [_c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_i64,
                                      _c_i64, _vp]),
     "finom_grid2d_destroy": (_c_int, [_vp]),
@@ -248,8 +255,7 @@ class Grid:
 
 def _dev(a):
     import torch
-    return None if a is None else torch.from_numpy(
-        np.ascontiguousarray(a, dtype=np.float64)).cuda()
+    return None if a is None else torch.from_numpy(np.array(a, dtype=np.float64)).cuda()
 
 
 def dense1d(x, y, a, b, eps, phi=None, psi=None):
