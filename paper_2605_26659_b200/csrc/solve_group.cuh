@@ -26,11 +26,14 @@ constexpr int GW = 16;                  // warps per CTA
 constexpr int GTHR = 32 * GW;
 constexpr int WREG = WST > WSM ? WST : WSM;  // shared doubles per warp (step / absorb)
 
+struct GX;
 struct GroupArgs {
   Dev d;
   double *S4;       // per tile: incoming (p, acc, q, accb) of the current half
   int *queue;       // [0]: next problem
-  int g;            // warps per problem (1, 2, 4, 8, 16)
+  int g;            // warps per problem (1, 2, 4, 8, 16; cluster form: up to 256)
+  GX *gxg;          // cluster form: exchange slots, g per cluster (global)
+  long long gxstride;  // (unused by this loop form)
   double *a_out, *b_out;
   long long *info;
 };
@@ -43,10 +46,76 @@ struct GX {
   int prob, pad;
 };
 
-__device__ __forceinline__ void group_sync(int id, int nthr) {
-  if (nthr == 32) __syncwarp();
-  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");
+// A problem's group: g warps, this one is warp j.  CTA groups (g <= 16)
+// synchronize with a named barrier and exchange through shared memory;
+// cluster groups (a small problem spread over a thread-block cluster, up to
+// 16 CTAs) with the cluster barrier and a global scratch (L2).
+struct Grp {
+  int g, j, bar;
+  bool cluster;
+  GX *gx;
+  __device__ __forceinline__ void sync() const {
+    if (cluster) {
+      __threadfence();  // (gx lives in global memory)
+      asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                   ::: "memory");
+    } else if (g == 1) {
+      __syncwarp();
+    } else {
+      asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * g) : "memory");
+    }
+  }
+};
+__device__ __forceinline__ Tf ld_tf(const Tf *p, bool global) {
+  return global ? ldcg_tf(p) : *p;
 }
+__device__ __forceinline__ double ld_d(const double *p, bool global) {
+  return global ? __ldcg(p) : *p;
+}
+
+// The states entering warp j of the group from the totals gx[0..g) of every
+// warp: the composition of warps 0..j-1 (forward) / g-1..j+1 (backward)
+// applied to the problem's zero boundary states, 32 warps per warp scan.
+__device__ __forceinline__ void group_prefix(const Grp &G, int lane, double &p, double &acc,
+                                             double &q, double &accb) {
+  const int g = G.g, j = G.j;
+  double sp = 0.0, sa = 0.0;
+  for (int c = 0; c < g; c += 32) {
+    const int k = c + lane;
+    const Tf f = k < g ? ld_tf(&G.gx[k].f, G.cluster) : tf_id();
+    Tf xf, xb, tf_, tb_;
+    warp_scan2<true>(f, tf_id(), xf, xb, tf_, tb_);
+    double pp = sp, aa = sa;
+    tf_apply_g(xf, pp, aa);
+    const int src = min(max(j - c, 0), 31);
+    pp = __shfl_sync(0xffffffffu, pp, src);
+    aa = __shfl_sync(0xffffffffu, aa, src);
+    if (j >= c && j < c + 32) {
+      p = pp;
+      acc = aa;
+    }
+    tf_apply_g(tf_, sp, sa);
+  }
+  double sq = 0.0, sb = 0.0;
+  const int nch = (g + 31) / 32;
+  for (int ci = nch - 1; ci >= 0; --ci) {
+    const int c = 32 * ci, k = c + lane;
+    const Tf b = k < g ? ld_tf(&G.gx[k].b, G.cluster) : tf_id();
+    Tf xf, xb, tf_, tb_;
+    warp_scan2<true>(tf_id(), b, xf, xb, tf_, tb_);
+    double qq = sq, bb = sb;
+    tf_apply_g(xb, qq, bb);
+    const int src = min(max(j - c, 0), 31);
+    qq = __shfl_sync(0xffffffffu, qq, src);
+    bb = __shfl_sync(0xffffffffu, bb, src);
+    if (j >= c && j < c + 32) {
+      q = qq;
+      accb = bb;
+    }
+    tf_apply_g(tb_, sq, sb);
+  }
+}
+
 
 // Per-tile incoming states of one half for tiles [b, e) of the warp (the
 // warp's share of its problem): lane chunks composed sequentially, a warp
@@ -54,8 +123,10 @@ __device__ __forceinline__ void group_sync(int id, int nthr) {
 // into S4 (lane-sequential).  Maps: R.lev[0] (written by the previous half's
 // epilogue or by the table build), forward composed left to right, backward
 // right to left; guarded compositions (a structural zero stays zero).
-__device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, int e, int j,
-                                              int g, GX *gx, int bar, int lane) {
+__device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, int e,
+                                           const Grp &G, int lane) {
+  const int g = G.g, j = G.j;
+  GX *gx = G.gx;
   const Node *nd = R.lev[0];
   const int n = e - b;
   const int L = (n + 31) / 32;
@@ -71,12 +142,16 @@ __device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, 
       gx[j].f = totf;
       gx[j].b = totb;
     }
-    group_sync(bar, 32 * g);
+    G.sync();
     // the totals of the group's earlier warps (forward) and later warps
     // (backward), applied to the problem's zero boundary states
-    for (int k = 0; k < j; ++k) tf_apply_g(gx[k].f, p, acc);
-    for (int k = g - 1; k > j; --k) tf_apply_g(gx[k].b, q, accb);
-    group_sync(bar, 32 * g);  // (gx is rewritten by the partials below)
+    if (g <= 16) {
+      for (int k = 0; k < j; ++k) tf_apply_g(ld_tf(&gx[k].f, G.cluster), p, acc);
+      for (int k = g - 1; k > j; --k) tf_apply_g(ld_tf(&gx[k].b, G.cluster), q, accb);
+    } else {
+      group_prefix(G, lane, p, acc, q, accb);
+    }
+    G.sync();  // (gx is rewritten by the partials below)
   }
   tf_apply_g(xf, p, acc);
   tf_apply_g(xb, q, accb);
@@ -109,6 +184,14 @@ __device__ __forceinline__ void group_prefetch(const Dev &d, int t, const TileSt
   const long long rb = HALF == 0 ? ts.yb : ts.xb, cb = HALF == 0 ? ts.xb : ts.yb;
   if (HALF == 0) l2_prefetch(d.PSI + rb, 8 * (size_t)nr);
   l2_prefetch((HALF == 0 ? d.PHI : d.PSI) + cb, 8 * (size_t)nc);
+}
+
+// The scalings and records the bulk copies read were written by this
+// kernel's generic stores (the previous half, a table rebuild): every lane
+// orders its stores before the async-proxy reads -- once per half / rebuild.
+__device__ __forceinline__ void proxy_fence() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncwarp();
 }
 
 // One half step of tile t with incoming states init = S4 + 4t (the k_step
@@ -153,31 +236,32 @@ __device__ __forceinline__ void group_tile(const Dev &d, int t, const TileStep &
   __syncwarp();
 #ifdef FB_DBG_PHASE
   long long ph_t0 = 0;
-  tile_compute<HALF, true>(d, in, tf_id(), lane, ph_t0, nullptr, part, true, st0, st1);
+  tile_compute<HALF, true, false>(d, in, tf_id(), lane, ph_t0, nullptr, part, true, st0, st1);
 #else
-  tile_compute<HALF, true>(d, in, tf_id(), lane, nullptr, part, true, st0, st1);
+  tile_compute<HALF, true, false>(d, in, tf_id(), lane, nullptr, part, true, st0, st1);
 #endif
 }
 
 // Partials of the warp's tiles (in tile order) -> the group's (in warp order).
-__device__ __noinline__ void group_partials(double (&pw)[4], int j, int g, GX *gx, int bar,
-                                               int lane) {
+__device__ __noinline__ void group_partials(double (&pw)[4], const Grp &G, int lane) {
+  const int g = G.g, j = G.j;
+  GX *gx = G.gx;
   if (g == 1) return;
   if (lane == 0)
     for (int k = 0; k < 4; ++k) gx[j].part[k] = pw[k];
-  group_sync(bar, 32 * g);
+  G.sync();
   double e = 0.0, mx = 0.0, mn = INFINITY, fl = -1.0;
   for (int k = 0; k < g; ++k) {
-    e = __dadd_rn(e, gx[k].part[0]);
-    mx = fmax(mx, gx[k].part[1]);
-    mn = fmin(mn, gx[k].part[2]);
-    fl = fmax(fl, gx[k].part[3]);
+    e = __dadd_rn(e, ld_d(&gx[k].part[0], G.cluster));
+    mx = fmax(mx, ld_d(&gx[k].part[1], G.cluster));
+    mn = fmin(mn, ld_d(&gx[k].part[2], G.cluster));
+    fl = fmax(fl, ld_d(&gx[k].part[3], G.cluster));
   }
   pw[0] = e;
   pw[1] = mx;
   pw[2] = mn;
   pw[3] = fl;
-  group_sync(bar, 32 * g);
+  G.sync();
 }
 
 // The table (re)build of the warp's tiles, out of line: it runs at the start
@@ -191,6 +275,11 @@ __device__ __noinline__ void group_build(const Dev &d, int build, int b, int e, 
   }
 }
 
+// CLUSTER = false: groups of g <= 16 warps inside a CTA, problems from the
+// queue.  CLUSTER = true: a thread-block cluster per problem (problem =
+// cluster index), its warps one group (a.g = warps per CTA x cluster size),
+// exchange through a.gxg (global, g entries per cluster).
+template <bool CLUSTER>
 __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double2 tab[64];
@@ -201,19 +290,40 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
   __syncthreads();
   const Dev &d = a.d;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = a.g, j = warp % g, grp = warp / g;
-  const int bar = 1 + grp;  // named barrier of the group (g > 1)
-  GX *gx = gxs + grp * g;
+  const int nw = blockDim.x >> 5;
+  Grp G;
+  G.cluster = CLUSTER;
+  int grp = 0, crank = 0, cid = 0;
+  if (CLUSTER) {
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+    G.g = a.g;
+    G.j = crank * nw + warp;
+    G.bar = 0;
+    G.gx = a.gxg + (size_t)cid * a.g;
+  } else {
+    G.g = a.g;
+    G.j = warp % a.g;
+    grp = warp / a.g;
+    G.bar = 1 + grp;  // named barrier of the group (g > 1)
+    G.gx = gxs + grp * a.g;
+  }
+  const int g = G.g, j = G.j;
   double *wsm = smem + (size_t)warp * WREG;
   unsigned long long *mb = mbar + warp;
   if (lane == 0) bar_init(mb);
   __syncwarp();
   unsigned phase = 0;
-  for (;;) {
-    if (j == 0 && lane == 0) gprob[grp] = atomicAdd(a.queue, 1);
-    group_sync(bar, 32 * g);
-    const int prob = gprob[grp];
-    group_sync(bar, 32 * g);
+  for (int round = 0;; ++round) {
+    int prob;
+    if (CLUSTER) {
+      prob = round == 0 ? cid : d.P;  // one problem per cluster
+    } else {
+      if (j == 0 && lane == 0) gprob[grp] = atomicAdd(a.queue, 1);
+      G.sync();
+      prob = gprob[grp];
+      G.sync();
+    }
     if (prob >= d.P) break;
     const ProbDesc &P = d.probs[prob];
     const int b = P.tile0 + (int)((long long)P.ntiles * j / g);
@@ -231,16 +341,17 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         d.B[0][P.yoff + k] = 0.0;
       }
     }
-    group_sync(bar, 32 * g);
+    G.sync();
     // tables of the initial kernel, half A's maps for the initial phi
     group_build(d, 1, b, e, wsm, tab, 0, false);
-    group_sync(bar, 32 * g);
+    G.sync();
     int it = 0, status = 0, fail_it = 0, sbuf = 0, n_abs = 0, converged = 0;
     bool absorbed = false;
-    double err = 0.0, psmax = 0.0, psmin = INFINITY;
+    double err = 0.0;
     for (;;) {
       // ---- half A: psi <- v / K'^T phi (_kernels.py:278-314)
-      group_carries(d.RA, a.S4, b, e, j, g, gx, bar, lane);
+      proxy_fence();
+      group_carries(d.RA, a.S4, b, e, G, lane);
       double pw[4] = {0.0, 0.0, INFINITY, -1.0};
       TileStep ts = d.steps[b < e ? b : 0];
       for (int t = b; t < e; ++t) {
@@ -253,10 +364,9 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         pw[2] = fmin(pw[2], pt[2]);
         pw[3] = fmax(pw[3], pt[3]);
       }
-      group_partials(pw, j, g, gx, bar, lane);
+      group_partials(pw, G, lane);
       err = pw[0];
-      psmax = pw[1];
-      psmin = pw[2];
+      const bool ps_oor = pw[1] > 0.0;  // (epi_rows<.., EXT = false>: out-of-range flag)
       if (j == 0 && lane == 0) d.hist[(long long)prob * d.itr_max + it] = err;
       if (pw[3] >= 0.0) {  // solver.py:177-184 (failure in half A)
         const long long fl = (long long)pw[3];
@@ -266,8 +376,9 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         break;
       }
       // ---- half B: phi <- u / K' psi (_kernels.py:315-349)
-      group_sync(bar, 32 * g);  // every psi of the problem is final
-      group_carries(d.RB, a.S4, b, e, j, g, gx, bar, lane);
+      G.sync();  // every psi of the problem is final
+      proxy_fence();
+      group_carries(d.RB, a.S4, b, e, G, lane);
       double qw[4] = {0.0, 0.0, INFINITY, -1.0};
       TileStep ts1 = d.steps[b < e ? b : 0];
       for (int t = b; t < e; ++t) {
@@ -279,8 +390,8 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         qw[2] = fmin(qw[2], pt[2]);
         qw[3] = fmax(qw[3], pt[3]);
       }
-      group_partials(qw, j, g, gx, bar, lane);
-      const double phmax = qw[1], phmin = qw[2];
+      group_partials(qw, G, lane);
+      const bool ph_oor = qw[1] > 0.0;
       const int k = ++it;  // solver.py:177
       if (qw[3] >= 0.0) {
         const long long fl = (long long)qw[3];
@@ -292,14 +403,13 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         converged = 1;
         break;
       }
-      if (d.stabilize && (phmax > d.hi_cut || psmax > d.hi_cut || phmin < d.lo_cut ||
-                          psmin < d.lo_cut)) {  // solver.py:193-198: absorb, phi = psi = 1
+      if (d.stabilize && (ph_oor || ps_oor)) {  // solver.py:193-198: absorb, phi = psi = 1
         if (j == 0 && lane == 0 && d.absorb_its)
           d.absorb_its[(long long)prob * d.itr_max + n_abs] = k;
         n_abs += 1;
-        group_sync(bar, 32 * g);  // every phi of the problem is final
+        G.sync();  // every phi of the problem is final
         group_build(d, 0, b, e, wsm, tab, sbuf, absorbed);
-        group_sync(bar, 32 * g);  // every tile has read the old shifts and scalings
+        G.sync();  // every tile has read the old shifts and scalings
         sbuf ^= 1;
         absorbed = true;
         if (e > b) {
@@ -310,7 +420,7 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         __syncwarp();
       }
       if (k >= d.itr_max) break;
-      group_sync(bar, 32 * g);  // every phi / half-A map of the problem is final
+      G.sync();  // every phi / half-A map of the problem is final
     }
     // ---- k_final's part: shifts out, info, control block
     const double *As = d.A[sbuf], *Bs = d.B[sbuf];
@@ -340,7 +450,7 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
       c.err = err;
       d.ctl[prob] = c;
     }
-    group_sync(bar, 32 * g);
+    G.sync();
   }
 }
 

@@ -320,15 +320,19 @@ __global__ void k_sq_seg_tot(SqArgs a, double *out) {
   }
 }
 
-// The sweep: CTA = tile t of WPC consecutive lines; lane l walks points
-// 8l .. 8l+7 of its warp's tile.  Lane maps of both recurrences, two warp
-// scans (the tile's incoming P / Q folded into the end lanes), the final
-// recurrences in the reference's operation order ((r * p) + acc, p + q),
-// then the CTA writes the rows transposed (four lines per 32-byte sector).
-__global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
-  __shared__ double so[WPC][SQX];  // input staging, then the tile's outputs
+// The sweep: CTA = tile t of LPC consecutive lines (a warp per line); lane l
+// walks points 8l .. 8l+7 of its warp's tile.  Lane maps of both
+// recurrences, two warp scans (the tile's incoming P / Q folded into the end
+// lanes), the final recurrences in the reference's operation order
+// ((r * p) + acc, p + q), then the CTA writes the rows transposed: LPC
+// consecutive doubles of every output row (LPC = 16: whole 128-byte lines;
+// 4: 32-byte sectors).
+template <int LPC>
+__global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
+  constexpr int THR = 32 * LPC;
+  __shared__ double so[LPC][SQX];  // input staging, then the tile's outputs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x % a.tl, p0 = (blockIdx.x / a.tl) * WPC, p = p0 + warp;
+  const int t = blockIdx.x % a.tl, p0 = (blockIdx.x / a.tl) * LPC, p = p0 + warp;
   griddep_wait();
   if (p < a.lines) {
     const size_t tile = (size_t)p * a.tl + t;
@@ -407,8 +411,8 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
   __syncthreads();
   const int cnt = min(SQT, a.n - t * SQT);
   if (!a.ew) {
-    for (int k = threadIdx.x; k < cnt * WPC; k += NTHR) {
-      const int i = k / WPC, w = k % WPC;
+    for (int k = threadIdx.x; k < cnt * LPC; k += THR) {
+      const int i = k / LPC, w = k % LPC;
       if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = so[w][i];
     }
     griddep_launch();
@@ -419,20 +423,20 @@ __global__ void __launch_bounds__(NTHR) k_sq_apply(SqArgs a) {
   double err = 0.0, vmax = 0.0, vmin = INFINITY;
   long long fail = LLONG_MAX;
   // every load of the thread's elements is issued before the first use
-  constexpr int EPER = SQT * WPC / NTHR;
+  constexpr int EPER = SQT * LPC / THR;
   double wq[EPER], sq[EPER];
 #pragma unroll
   for (int q = 0; q < EPER; ++q) {
-    const int k = threadIdx.x + q * NTHR, i = k / WPC, w = k % WPC;
-    const bool live = k < cnt * WPC && p0 + w < a.lines;
+    const int k = threadIdx.x + q * THR, i = k / LPC, w = k % LPC;
+    const bool live = k < cnt * LPC && p0 + w < a.lines;
     const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
     wq[q] = live ? __ldcs(a.ew + idx) : 0.0;
     sq[q] = live && a.eerr ? __ldcs(a.esc + idx) : 0.0;
   }
 #pragma unroll
   for (int q = 0; q < EPER; ++q) {
-    const int k = threadIdx.x + q * NTHR, i = k / WPC, w = k % WPC;
-    if (k >= cnt * WPC || p0 + w >= a.lines) continue;
+    const int k = threadIdx.x + q * THR, i = k / LPC, w = k % LPC;
+    if (k >= cnt * LPC || p0 + w >= a.lines) continue;
     const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
     // flat index of the whole grid (a row shard holds rows [ek0, ek0 + lines) of eng)
     const long long kg = a.ek0 + p0 + w + (long long)a.eng * (t * SQT + i);

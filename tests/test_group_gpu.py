@@ -76,3 +76,32 @@ def test_group_matches_tile_parallel_loop(monkeypatch):
             assert list(sa.absorb_iterations) == list(sr.absorb_iterations)
             assert rel_inf(sa.phi, sr.phi) < 1e-10 and rel_inf(sa.psi, sr.psi) < 1e-10
             assert abs(sa.cost - sr.cost) <= 1e-10 * abs(sr.cost)
+
+
+@pytest.fixture
+def cluster(monkeypatch):
+    """The cluster form (a thread-block cluster per problem) on small problems."""
+    monkeypatch.setenv("FB_GROUP", "0")
+    monkeypatch.setenv("FB_CLUSTER", "1")
+
+
+def test_cluster_solver_cases_vs_reference(cluster):
+    T.test_solver_cases_vs_reference()
+
+
+def test_cluster_failure_diagnostics(cluster):
+    T.test_failure_diagnostics()
+
+
+def test_cluster_config1_vs_reference(cluster):
+    T.test_config1_vs_reference()
+
+
+def test_cluster_mixed_sizes_vs_oracle(cluster):
+    T.test_batched_mixed_sizes_vs_oracle()
+
+
+def test_cluster_tol_stops_per_problem(monkeypatch):
+    monkeypatch.setenv("FB_GROUP", "0")
+    monkeypatch.setenv("FB_CLUSTER", "1")
+    T.test_batched_tol_stops_per_problem(monkeypatch, "1")
