@@ -95,8 +95,19 @@ int finom_solve1d(finom_plan1d *plan, const double *u_dev, const double *v_dev,
                   int64_t itr_max, double tol, int stabilize, double absorb_threshold,
                   double *hist_dev, int64_t *info_dev, int64_t *absorb_its_dev, void *stream);
 
+/* finom_solve1d without waiting for the device: returns 0 once the loop is
+ * queued on `stream` (or an error >= 100); each problem's status is
+ * info_dev[5 p + 2] when the stream has run.  The batched API's pipeline
+ * queues chunk k's solve and stages chunk k + 1 while it runs. */
+int finom_solve1d_async(finom_plan1d *plan, const double *u_dev, const double *v_dev,
+                        double *phi_dev, double *psi_dev, double *a_dev, double *b_dev,
+                        int64_t itr_max, double tol, int stabilize, double absorb_threshold,
+                        double *hist_dev, int64_t *info_dev, int64_t *absorb_its_dev,
+                        void *stream);
+
 /* transport_cost_fast (solver.py:252-271) per problem, with the shifts
- * a_dev/b_dev (nullable = zero) folded into the kernel. cost_dev: P doubles. */
+ * a_dev/b_dev (nullable = zero) folded into the kernel. cost_dev: P doubles,
+ * final once `stream` has run (no host wait inside). */
 int finom_cost1d(finom_plan1d *plan, const double *a_dev, const double *b_dev,
                  const double *phi_dev, const double *psi_dev, double *cost_dev, void *stream);
 

@@ -32,6 +32,8 @@ SIGNATURES = {
     "finom_plan1d_info": (_c_int, [_vp, _vp]),
     "finom_solve1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int,
                                _c_dbl, _vp, _vp, _vp, _vp]),
+    "finom_solve1d_async": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int,
+                                     _c_dbl, _vp, _vp, _vp, _vp]),
     "finom_cost1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "finom_apply1d": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _vp, _vp]),
     "finom_iterate1d": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -286,11 +286,14 @@ class BatchSolver1D:
             self.abs_its = torch.zeros(self.P * itr, dtype=torch.int64, device=dev)
             self._itr = itr
 
-    def solve(self, itr_max, tol=0.0, stabilize=True, absorb_threshold=200.0):
-        """Run the device loop; returns the worst status (0/1/2). No host sync inside."""
+    def solve(self, itr_max, tol=0.0, stabilize=True, absorb_threshold=200.0, sync=True):
+        """Run the device loop on the current stream; returns the worst status
+        (0/1/2) -- or, with sync=False, 0 as soon as the loop is queued (the
+        per-problem status is then info[5 p + 2] once the stream has run)."""
         self._bufs(int(itr_max))
         lib = _lib.load()
-        return _lib.check(lib.finom_solve1d(
+        fn = lib.finom_solve1d if sync else lib.finom_solve1d_async
+        return _lib.check(fn(
             self.plan.handle, _lib.ptr(self.u), _lib.ptr(self.v), _lib.ptr(self.phi),
             _lib.ptr(self.psi), _lib.ptr(self.a), _lib.ptr(self.b), int(itr_max), float(tol),
             int(bool(stabilize)), float(absorb_threshold), _lib.ptr(self.hist),
@@ -304,43 +307,112 @@ class BatchSolver1D:
         return self.cost
 
 
+def _pipeline_ranges(sizes):
+    """Problem ranges of the batched API's pipeline stages: about 1/6 of the
+    batch each (>= 256 problems and >= 2^22 points per stage), one stage for
+    small batches.  FINOM_PIPE_STAGES overrides the stage count.  (Config 5,
+    8192 x 16384, warm calls: 1 stage 1.53 s, 4: 1.22-1.25, 6: 1.20-1.24,
+    8: 1.25, 12: 1.30 -- each stage's own loop has a tail, so more stages
+    than needed to hide the transfers cost time.)"""
+    P, pts = len(sizes), int(np.sum(sizes))
+    k = min(6, P // 256, pts >> 22)
+    env = os.environ.get("FINOM_PIPE_STAGES")
+    if env:
+        k = int(env)
+    k = max(1, min(k, P))
+    return [(P * i // k, P * (i + 1) // k) for i in range(k)]
+
+
 def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
     """Batch of independent sinkhorn_1d problems in one device loop.
 
     ``config`` supplies itr_max / tol / stabilize / threshold / cadence for all
     problems; ``epsilons`` (optional) overrides config.epsilon per problem.
     Raises the reference's exception if any problem fails.
+
+    Large batches run as a pipeline of stages (problem ranges): stage k + 1's
+    plan and host -> device staging (a copy stream) and stage k - 1's results
+    device -> host run while stage k's loop runs on the compute stream, so the
+    transfers and host-side tiling hide behind the device loop.  Every problem
+    is solved exactly as in a single-stage call (problems are independent).
     """
-    eps = config.epsilon if epsilons is None else epsilons
-    verbose = os.environ.get("FB_VERBOSE")
-    t0 = perf_counter()
-    bs = BatchSolver1D(xs, ys, us, vs, eps)
-    setup = perf_counter() - t0
-    t1 = perf_counter()
-    status = bs.solve(config.itr_max, config.tol, config.stabilize, config.absorb_threshold)
-    info = bs.info.view(bs.P, 5).cpu().numpy()
-    loop = perf_counter() - t1
-    raise_status(status)
-    bs.compute_cost()
     import torch
-    torch.cuda.synchronize()
+    if not (len(xs) == len(ys) == len(us) == len(vs)):
+        raise DimensionMismatch("xs, ys, us, vs must have one entry per problem")
+    P = len(xs)
+    eps = np.broadcast_to(np.asarray(config.epsilon if epsilons is None else epsilons,
+                                     dtype=np.float64), (P,))
+    verbose = os.environ.get("FB_VERBOSE")
+    node = lambda z: z.nodes if hasattr(z, "nodes") else np.asarray(z, dtype=np.float64)
+    nx = np.array([len(node(x)) for x in xs], dtype=np.int64)
+    ny = np.array([len(node(y)) for y in ys], dtype=np.int64)
+    xoff = np.zeros(P + 1, dtype=np.int64)
+    yoff = np.zeros(P + 1, dtype=np.int64)
+    xoff[1:] = np.cumsum(nx)
+    yoff[1:] = np.cumsum(ny)
+    itr = int(config.itr_max)
+    # the batch's results, filled stage by stage (device -> host through the pinned staging)
+    phi = np.empty(int(xoff[-1]))
+    psi = np.empty(int(yoff[-1]))
+    a = np.empty(int(xoff[-1]))
+    b = np.empty(int(yoff[-1]))
+    hist = np.empty((P, itr))
+    abs_its = np.empty((P, itr), dtype=np.int64)
+    info = np.empty((P, 5), dtype=np.int64)
+    cost = np.empty(P)
+    comp = torch.cuda.current_stream()
+    t0 = perf_counter()
+    setup = [0.0]
 
-    def host(t):  # device tensor -> host through the pinned staging
-        h = np.empty(t.numel(), dtype=np.float64 if t.dtype == torch.float64 else np.int64)
-        _lib.stage_copy(1, h, t)
-        return h
+    def fetch(stage):
+        lo, hi, bs, done = stage
+        done.synchronize()
+        x0, x1, y0, y1 = xoff[lo], xoff[hi], yoff[lo], yoff[hi]
+        for h, d in ((phi[x0:x1], bs.phi), (psi[y0:y1], bs.psi), (a[x0:x1], bs.a),
+                     (b[y0:y1], bs.b), (hist[lo:hi].reshape(-1), bs.hist),
+                     (abs_its[lo:hi].reshape(-1), bs.abs_its), (info[lo:hi].reshape(-1), bs.info),
+                     (cost[lo:hi], bs.cost)):
+            _lib.stage_copy(1, h, d)
 
-    t2 = perf_counter()
-    hist = host(bs.hist).reshape(bs.P, -1)
-    abs_its = host(bs.abs_its).reshape(bs.P, -1)
-    cost = bs.cost.cpu().numpy()
-    phi, psi, a, b = host(bs.phi), host(bs.psi), host(bs.a), host(bs.b)
-    t3 = perf_counter()
-    sols = BatchSolutions(xs, ys, bs.plan.xoff, bs.plan.yoff, bs.eps, config, info, cost,
-                          phi, psi, a, b, hist, abs_its, setup + loop, setup)
+    pending = None
+    stages = []  # (kept to the end: destroying a plan waits for every stream it ran on)
+    for lo, hi in _pipeline_ranges(nx):
+        ts = perf_counter()
+        # plan (host tiling + H2D) and weights on a stream of the stage's own:
+        # nothing queued on it can make its pageable copies wait for the
+        # stages before (whose kernels wait for the SMs the running loop holds)
+        copy = torch.cuda.Stream()
+        with torch.cuda.stream(copy):
+            bs = BatchSolver1D(xs[lo:hi], ys[lo:hi], us[lo:hi], vs[lo:hi], eps[lo:hi])
+            bs._bufs(itr)
+            ready = torch.cuda.Event()
+            ready.record(copy)
+        tp = perf_counter()
+        setup[0] += tp - ts
+        comp.wait_event(ready)
+        for t in (bs.u, bs.v, bs.phi, bs.psi, bs.a, bs.b, bs.cost, bs.hist, bs.info, bs.abs_its):
+            t.record_stream(comp)
+        bs.solve(itr, config.tol, config.stabilize, config.absorb_threshold, sync=False)
+        bs.compute_cost()
+        done = torch.cuda.Event()
+        done.record(comp)
+        tq = perf_counter()
+        if pending is not None:
+            fetch(pending)
+        if verbose:
+            print("  stage %d-%d: prep %.1f ms, queue %.1f ms, fetch (previous) %.1f ms" % (
+                lo, hi, 1e3 * (tp - ts), 1e3 * (tq - tp), 1e3 * (perf_counter() - tq)), flush=True)
+        pending = (lo, hi, bs, done)
+        stages.append(bs)
+    fetch(pending)
+    wall = perf_counter() - t0
+    del stages, bs, pending
+    raise_status(int(info[:, 2].max()) if P else 0)
+    sols = BatchSolutions(xs, ys, xoff, yoff, np.array(eps), config, info, cost,
+                          phi, psi, a, b, hist, abs_its, wall, setup[0])
     if verbose:
-        print("sinkhorn_1d_batched: setup %.1f loop %.1f cost+d2h %.1f ms" % (
-            1e3 * setup, 1e3 * loop, 1e3 * (t3 - t2)), flush=True)
+        print("sinkhorn_1d_batched: %d stage(s), setup %.1f ms, call %.1f ms" % (
+            len(_pipeline_ranges(nx)), 1e3 * setup[0], 1e3 * wall), flush=True)
     return sols
 
 
