@@ -151,7 +151,8 @@ __device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, 
     } else {
       group_prefix(G, lane, p, acc, q, accb);
     }
-    G.sync();  // (gx is rewritten by the partials below)
+    // (no barrier: the partials write other fields of gx, and the next
+    // writes of f / b come after the partials' barrier)
   }
   tf_apply_g(xf, p, acc);
   tf_apply_g(xb, q, accb);
@@ -222,6 +223,8 @@ __device__ __forceinline__ void group_tile(const Dev &d, int t, const TileStep &
     bulk_rec(in.rec, d.TR[HALF] + (size_t)t * TREC, rbytes, bar);
     vec_issue(in.rold, Rs, vr, bar);
     vec_issue(in.cv, Cs, vc, bar);
+    // (measured at config 5: prefetch distance 2 1074 ms, record only
+    // 1050, distance 1 with the vectors 1047 ms per solve)
     if (next) group_prefetch<HALF>(d, t + 1, nts);
   }
   // lanes 0 / 4: the incoming states (forward / backward), off the walk's path
@@ -251,17 +254,38 @@ __device__ __noinline__ void group_partials(double (&pw)[4], const Grp &G, int l
     for (int k = 0; k < 4; ++k) gx[j].part[k] = pw[k];
   G.sync();
   double e = 0.0, mx = 0.0, mn = INFINITY, fl = -1.0;
-  for (int k = 0; k < g; ++k) {
-    e = __dadd_rn(e, ld_d(&gx[k].part[0], G.cluster));
-    mx = fmax(mx, ld_d(&gx[k].part[1], G.cluster));
-    mn = fmin(mn, ld_d(&gx[k].part[2], G.cluster));
-    fl = fmax(fl, ld_d(&gx[k].part[3], G.cluster));
+  if (g <= 16) {  // (shared memory: warp order)
+    for (int k = 0; k < g; ++k) {
+      e = __dadd_rn(e, ld_d(&gx[k].part[0], G.cluster));
+      mx = fmax(mx, ld_d(&gx[k].part[1], G.cluster));
+      mn = fmin(mn, ld_d(&gx[k].part[2], G.cluster));
+      fl = fmax(fl, ld_d(&gx[k].part[3], G.cluster));
+    }
+  } else {
+    // large (cluster) groups: the lanes load the partials in parallel (one
+    // round of loads per 32 warps instead of g dependent rounds), then fixed
+    // butterfly reductions -- a fixed order for a given g.  (config 1 with
+    // FB_CLUSTER=1: 68.6 -> 46.6 us per iteration)
+    for (int c = 0; c < g; c += 32) {
+      const int k = c + lane;
+      if (k < g) {
+        e = __dadd_rn(e, ld_d(&gx[k].part[0], G.cluster));
+        mx = fmax(mx, ld_d(&gx[k].part[1], G.cluster));
+        mn = fmin(mn, ld_d(&gx[k].part[2], G.cluster));
+        fl = fmax(fl, ld_d(&gx[k].part[3], G.cluster));
+      }
+    }
+    e = warp_sum(e);
+    mx = warp_max(mx);
+    mn = warp_min(mn);
+    fl = warp_max(fl);
   }
   pw[0] = e;
   pw[1] = mx;
   pw[2] = mn;
   pw[3] = fl;
-  G.sync();
+  // (no barrier: the next writes of the partials come after the next
+  // half's barriers)
 }
 
 // The table (re)build of the warp's tiles, out of line: it runs at the start
@@ -364,6 +388,7 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         pw[2] = fmin(pw[2], pt[2]);
         pw[3] = fmax(pw[3], pt[3]);
       }
+      pw[0] = warp_sum(pw[0]);  // (lane partials of the warp's tiles, in tile order per lane)
       group_partials(pw, G, lane);
       err = pw[0];
       const bool ps_oor = pw[1] > 0.0;  // (epi_rows<.., EXT = false>: out-of-range flag)

@@ -8,6 +8,9 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_26659_b200 import _lib  # noqa: E402
+if os.environ.get("FINOM_LIB"):  # (timing a library variant)
+    _lib.LIB_PATH = os.path.abspath(os.environ["FINOM_LIB"])
 import paper_2605_26659_b200 as fb  # noqa: E402
 from paper_2605_26659_b200 import workloads as W  # noqa: E402
 
@@ -29,5 +32,5 @@ for _ in range(reps):
     ts.append(e0.elapsed_time(e1))
 ms = float(np.median(ts))
 info = bs.info.view(bs.P, 5).cpu().numpy()
-print("B %d n %d its %d: %.3f ms/solve  %.3e pts*it/s  absorbs %d  group=%s" % (
-    B, n, its, ms, B * n * its / (ms * 1e-3), int(info[:, 3].sum()), os.environ.get("FB_GROUP", "auto")))
+print("%s B %d n %d its %d: %.3f ms/solve  %.3e pts*it/s  absorbs %d  group=%s" % (
+    os.path.basename(_lib.LIB_PATH), B, n, its, ms, B * n * its / (ms * 1e-3), int(info[:, 3].sum()), os.environ.get("FB_GROUP", "auto")))
