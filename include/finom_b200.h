@@ -307,6 +307,30 @@ int finom_grid2d_finish(finom_grid2d *g, int half, const double *in, const doubl
 int finom_grid2d_absorb(finom_grid2d *g, int side, double *shift, const double *W,
                         const double *SC_all, const int32_t *prv, const int32_t *nxt, int R, int r,
                         void *stream);
+/* Neighbour-only absorption exchange (replaces the all-gather of the whole
+ * scaling grids for finom_grid2d_absorb): solver._shift's np.interp fill
+ * (solver.py:135-153) reaches into another shard only at the last / first
+ * positive-mass point of that shard's segment of a column.
+ * finom_grid2d_edges writes this shard's m x 2 scalings at those points
+ * (lastpos / firstpos: local indices, -1 if the segment has no mass); the
+ * caller all-gathers them ([R][m][2]); finom_grid2d_absorb_nb updates the
+ * shift grid: prv_src / nxt_src per local point (>= 0 local index, <= -2
+ * segment -2 - src of the gathered edges, -1 none), prv_g / nxt_g the
+ * neighbours' flat indices in the whole grid. */
+int finom_grid2d_edges(finom_grid2d *g, const double *SC, const int32_t *lastpos,
+                       const int32_t *firstpos, int m, double *edges_out, void *stream);
+int finom_grid2d_absorb_nb(finom_grid2d *g, int side, double *shift, const double *W,
+                           const double *SC, const int32_t *prv_src, const int32_t *nxt_src,
+                           const int32_t *prv_g, const int32_t *nxt_g, const double *edges_all,
+                           void *stream);
+/* run_driver's decisions (solver.py:173-198) of a row-sharded iteration on
+ * the device: the all-gathered partials of both halves ([R][4] each, as
+ * finom_grid2d_finish writes them) combined in rank order; ctl (8 int64,
+ * zeroed before the loop): it, status, converged, absorb this iteration,
+ * done, n_absorb, failure code. */
+int finom_grid2d_decide(const double *parts_a, const double *parts_b, int R, int64_t *ctl,
+                        double *hist, int64_t *absorb_its, int64_t itr_max, double tol,
+                        int stabilize, double threshold, void *stream);
 
 #ifdef __cplusplus
 }

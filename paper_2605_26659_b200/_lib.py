@@ -80,6 +80,10 @@ SIGNATURES = {
     "finom_grid2d_xpre": (_c_int, [_vp, _c_int, _vp, _vp, _c_int, _vp, _vp]),
     "finom_grid2d_finish": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int,
                                      _vp, _vp, _vp, _vp]),
+    "finom_grid2d_edges": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _vp]),
+    "finom_grid2d_absorb_nb": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "finom_grid2d_decide": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int,
+                                     _c_dbl, _vp]),
     "finom_grid2d_absorb": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                      _vp]),
 }

@@ -308,14 +308,16 @@ class BatchSolver1D:
 
 
 def _pipeline_ranges(sizes):
-    """Problem ranges of the batched API's pipeline stages: about 1/6 of the
-    batch each (>= 256 problems and >= 2^22 points per stage), one stage for
-    small batches.  FINOM_PIPE_STAGES overrides the stage count.  (Config 5,
-    8192 x 16384, warm calls: 1 stage 1.53 s, 4: 1.22-1.25, 6: 1.20-1.24,
-    8: 1.25, 12: 1.30 -- each stage's own loop has a tail, so more stages
-    than needed to hide the transfers cost time.)"""
+    """Problem ranges of the batched API's pipeline stages: >= 1024 problems
+    and >= 2^22 points per stage, at most 8 stages, one stage for small
+    batches.  FINOM_PIPE_STAGES overrides the stage count.  (Config 5, 8192 x
+    16384, warm calls: 1 stage 1.53 s, 4: 1.22-1.25, 6: 1.20-1.24, 8: 1.25,
+    12: 1.30.  A stage's own loop needs enough problems to fill the GPU
+    evenly -- 1024 problems of g = 16 warps are 7 rounds of the 2368 resident
+    warps at 99 % occupancy, 256 would leave 14 % idle -- so a rank of an
+    8-way split (1024 problems) runs one stage.)"""
     P, pts = len(sizes), int(np.sum(sizes))
-    k = min(6, P // 256, pts >> 22)
+    k = min(8, P // 1024, pts >> 22)
     env = os.environ.get("FINOM_PIPE_STAGES")
     if env:
         k = int(env)

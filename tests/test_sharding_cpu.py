@@ -167,3 +167,42 @@ def test_row_shard_gather_gloo_world2():
     for rank, ok, comb in res:
         assert ok
         assert comb == (3.0, 1.0, 0.5, 6.0)
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_neighbour_index_of_row_shards(R):
+    """The neighbour-only absorption exchange: every zero-mass point's previous /
+    next positive-mass point of the whole grid (flat column-major order) is
+    either in its own shard or the last / first positive point of another
+    shard's segment of a column -- the only values the shards exchange."""
+    from paper_2605_26659_b200 import sharding as S
+    rng = np.random.default_rng(7)
+    n, m = 12, 9
+    w = rng.uniform(0.1, 1.0, n * m)
+    w[rng.random(n * m) < 0.55] = 0.0  # long zero-mass runs crossing shard segments
+    w[:5] = 0.0
+    w[-4:] = 0.0
+    prv, nxt = S._pos_index(w)
+    ranges = S.grid_row_ranges(n, R)
+    nbs = [S._nb_index(w, n, m, k0, k1) for k0, k1 in ranges]
+    nl = n // R
+
+    def flat_of(q, local):
+        return (local // nl) * n + ranges[q][0] + local % nl
+
+    for r, (k0, k1) in enumerate(ranges):
+        nb = nbs[r]
+        for k in range(nl * m):
+            kg = (k // nl) * n + k0 + k % nl
+            for src, g, want, key in ((nb["prv_src"][k], nb["prv_g"][k], prv[kg], "lastpos"),
+                                      (nb["nxt_src"][k], nb["nxt_g"][k], nxt[kg], "firstpos")):
+                if want < 0 or want >= n * m:
+                    assert src == -1
+                    continue
+                assert g == want
+                if src >= 0:
+                    assert flat_of(r, src) == want
+                else:
+                    seg = -2 - src
+                    q, col = seg // m, seg % m
+                    assert flat_of(q, nbs[q][key][col]) == want
