@@ -430,3 +430,223 @@ def sinkhorn_2d_row_sharded_sim(source, target, u, v, config, R):
         s.close()
     return _solution_2d(source, target, config, out["PHI"], out["PSI"], out["A"], out["B"], it,
                         conv, status, hist, abs_its, 0.0)
+
+
+
+# ---------------------------------------------------------------------------
+# Distributed 1D scan (BASELINE north star: "very long 1D meshes use a
+# distributed scan, where each GPU scans its segment and per-segment carries
+# are exchanged with a small NCCL all-gather over NVLink before a fix-up
+# pass").  Rank r owns segment r of the merged order x U y (merge-path
+# splits, finom_seg1d_*): per half its tile maps and resolve tree give the
+# segment's totals of both recurrences (_kernels.py:53-88), the totals are
+# all-gathered (10 doubles per rank), each rank composes those of the
+# segments before / after it into its incoming states and computes its rows
+# and their scaling update; the partials are all-gathered and combined in
+# rank order, so run_driver's decisions are identical on every rank.  An
+# absorption all-gathers the scalings (np.interp over the whole vector).
+
+def seg_split(x, y, R):
+    """Merge-path split points [(i_k, j_k)] k = 0..R of a 1D problem."""
+    from . import _lib
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    b = np.zeros(2 * (R + 1), dtype=np.int64)
+    _lib.check(_lib.load(False).finom_seg1d_split(x.size, _lib.ptr(x), y.size, _lib.ptr(y), R,
+                                                  _lib.ptr(b)), "finom_seg1d_split")
+    return [(int(b[2 * k]), int(b[2 * k + 1])) for k in range(R + 1)]
+
+
+def combine_parts_1d(parts):
+    """Rank-order combine of per-segment partials (err, max, min, status or -1):
+    errors summed in rank order, extremes, and the failure of the LAST failing
+    segment (the reference's loops run downward, _kernels.py:293-314)."""
+    parts = np.asarray(parts, dtype=np.float64).reshape(-1, 4)
+    err = 0.0
+    for e in parts[:, 0]:
+        err += float(e)
+    fails = [f for f in parts[:, 3] if f >= 0]
+    return err, float(np.max(parts[:, 1])), float(np.min(parts[:, 2])), (
+        float(fails[-1]) if fails else -1.0)
+
+
+class Segment1D:
+    """Device state of one segment (whole-length vectors, this rank's rows)."""
+
+    def __init__(self, x, y, u, v, eps, R, r):
+        import ctypes
+        import torch
+        from . import _lib
+        self._lib = _lib
+        self.lib = _lib.load()
+        x, y = (np.ascontiguousarray(z, dtype=np.float64) for z in (x, y))
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.finom_seg1d_create(x.size, _lib.ptr(x), y.size, _lib.ptr(y), eps, R, r,
+                                               _lib.stream_ptr(), ctypes.byref(h)),
+                   "finom_seg1d_create")
+        self.h = h
+        w = np.zeros(4, dtype=np.int64)
+        self.lib.finom_seg1d_window(h, _lib.ptr(w))
+        self.window = tuple(int(k) for k in w)
+        dev = torch.device("cuda")
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+        n, m = x.size, y.size
+        self.U, self.V = t(u), t(v)
+        self.PHI = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)  # solver.py:165-166
+        self.PSI = torch.full((m,), 1.0 / n, dtype=torch.float64, device=dev)
+        self.A = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.B = torch.zeros(m, dtype=torch.float64, device=dev)
+        self.tot = torch.zeros(10, dtype=torch.float64, device=dev)
+        self.part = torch.zeros(4, dtype=torch.float64, device=dev)
+        pu, nu = _pos_index(np.asarray(u))
+        pv, nv = _pos_index(np.asarray(v))
+        it = lambda a: torch.from_numpy(a).to(dev)
+        self.prvU, self.nxtU, self.prvV, self.nxtV = it(pu), it(nu), it(pv), it(nv)
+        self.shifted = False
+
+    def _sh(self):
+        return (self.A, self.B) if self.shifted else (None, None)
+
+    def pre(self, half):
+        L, P = self._lib, self._lib.ptr
+        a, b = self._sh()
+        L.check(self.lib.finom_seg1d_pre(self.h, half, P(self.PHI if half == 0 else self.PSI),
+                                         P(a), P(b), P(self.tot), L.stream_ptr()),
+                "finom_seg1d_pre")
+        return self.tot
+
+    def finish(self, half, tot_all):
+        L, P = self._lib, self._lib.ptr
+        a, b = self._sh()
+        inp, W, SC = (self.PHI, self.V, self.PSI) if half == 0 else (self.PSI, self.U, self.PHI)
+        L.check(self.lib.finom_seg1d_finish(self.h, half, P(inp), P(a), P(b), P(tot_all), P(W),
+                                            P(SC), P(self.part), L.stream_ptr()),
+                "finom_seg1d_finish")
+        return self.part
+
+    def absorb(self, side, sc_whole):
+        L, P = self._lib, self._lib.ptr
+        sh, W = (self.A, self.U) if side == 0 else (self.B, self.V)
+        prv, nxt = (self.prvU, self.nxtU) if side == 0 else (self.prvV, self.nxtV)
+        L.check(self.lib.finom_seg1d_absorb(self.h, side, P(sh), P(W), P(sc_whole), P(prv),
+                                            P(nxt), L.stream_ptr()), "finom_seg1d_absorb")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.finom_seg1d_destroy(self.h)
+            self.h = None
+
+
+def _assemble_1d(vectors, windows, side):
+    """Whole vector from per-segment copies: segment k's window of `side` (0: x, 1: y)."""
+    out = np.array(vectors[0], dtype=np.float64)
+    for vec, w in zip(vectors, windows):
+        lo, hi = (w[0], w[1]) if side == 0 else (w[2], w[3])
+        out[lo:hi] = np.asarray(vec)[lo:hi]
+    return out
+
+
+def _solution_1d(x, y, config, phi, psi, a, b, it, conv, status, hist, abs_its, wall):
+    import dataclasses
+    from . import kernel1d
+    from .mesh import Mesh1D
+    from .solver import Solution, history_from, raise_status, transport_cost_fast
+    raise_status(status)
+    X, Y = Mesh1D(x), Mesh1D(y)
+    op = kernel1d.KernelOperator1D(X, Y, config.epsilon, a, b,
+                                   kernel1d._PlanCache(X, Y, config.epsilon))
+    h = np.zeros(config.itr_max)
+    h[:len(hist)] = hist
+    sol = Solution(phi=phi, psi=psi, a=a, b=b, kernel=op, iterations_run=it, converged=conv,
+                   marginal_error_history=history_from(h, it, conv, config), wall_time=wall,
+                   setup_time=0.0, cost=float("nan"), config=config,
+                   absorb_iterations=list(abs_its))
+    return dataclasses.replace(sol, cost=float(transport_cost_fast(sol)))
+
+
+def sinkhorn_1d_segmented(x, y, u, v, config, group=None):
+    """sinkhorn_1d of ONE problem as a distributed scan over the process group
+    (one GPU per rank, NCCL).  Every rank passes the whole problem; returns
+    the Solution on every rank."""
+    import time
+    import torch
+    import torch.distributed as dist
+    X = np.asarray(getattr(x, "nodes", x), dtype=np.float64)
+    Y = np.asarray(getattr(y, "nodes", y), dtype=np.float64)
+    Uw = np.asarray(getattr(u, "weights", u), dtype=np.float64)
+    Vw = np.asarray(getattr(v, "weights", v), dtype=np.float64)
+    R, r = dist.get_world_size(group), dist.get_rank(group)
+    sg = Segment1D(X, Y, Uw, Vw, config.epsilon, R, r)
+    dev = sg.PHI.device
+    tot_all = torch.empty(10 * R, dtype=torch.float64, device=dev)
+    parts = torch.empty(4 * R, dtype=torch.float64, device=dev)
+
+    def phase(half, dyn):
+        dist.all_gather_into_tensor(tot_all, sg.pre(half).contiguous(), group=group)
+        dist.all_gather_into_tensor(parts, sg.finish(half, tot_all).contiguous(), group=group)
+        return combine_parts_1d(parts.cpu().numpy())
+
+    wins = [None] * R
+    dist.all_gather_object(wins, sg.window, group=group)
+
+    def gather_whole(t, side):
+        g = torch.empty(R * t.numel(), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(g, t.contiguous(), group=group)
+        return _assemble_1d(np.split(g.cpu().numpy(), R), wins, side)
+
+    def absorb():
+        for side, sc in ((0, sg.PHI), (1, sg.PSI)):
+            whole = torch.from_numpy(gather_whole(sc, side)).to(dev)
+            sg.absorb(side, whole)
+        sg.PHI.fill_(1.0)
+        sg.PSI.fill_(1.0)
+        sg.shifted = True
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    it, conv, status, hist, abs_its = run_driver_2d(phase, absorb, config)
+    torch.cuda.synchronize()
+    wall = max_over_ranks(time.perf_counter() - t0)
+    phi, psi = gather_whole(sg.PHI, 0), gather_whole(sg.PSI, 1)
+    a, b = sg.A.cpu().numpy(), sg.B.cpu().numpy()
+    sg.close()
+    return _solution_1d(X, Y, config, phi, psi, a, b, it, conv, status, hist, abs_its, wall)
+
+
+def sinkhorn_1d_segmented_sim(x, y, u, v, config, R):
+    """The distributed scan with R segments in ONE process on one GPU: the
+    segments' phases run one after another and the collectives are plain
+    concatenations (a correctness check of the decomposition; never a
+    timing)."""
+    import torch
+    X = np.asarray(getattr(x, "nodes", x), dtype=np.float64)
+    Y = np.asarray(getattr(y, "nodes", y), dtype=np.float64)
+    Uw = np.asarray(getattr(u, "weights", u), dtype=np.float64)
+    Vw = np.asarray(getattr(v, "weights", v), dtype=np.float64)
+    segs = [Segment1D(X, Y, Uw, Vw, config.epsilon, R, k) for k in range(R)]
+    wins = [s.window for s in segs]
+
+    def phase(half, dyn):
+        tot_all = torch.cat([s.pre(half).clone() for s in segs])
+        parts = [s.finish(half, tot_all).cpu().numpy() for s in segs]
+        return combine_parts_1d(parts)
+
+    def absorb():
+        for side in (0, 1):
+            vecs = [(s.PHI if side == 0 else s.PSI).cpu().numpy() for s in segs]
+            whole = torch.from_numpy(_assemble_1d(vecs, wins, side)).cuda()
+            for s in segs:
+                s.absorb(side, whole)
+        for s in segs:
+            s.PHI.fill_(1.0)
+            s.PSI.fill_(1.0)
+            s.shifted = True
+
+    it, conv, status, hist, abs_its = run_driver_2d(phase, absorb, config)
+    torch.cuda.synchronize()
+    phi = _assemble_1d([s.PHI.cpu().numpy() for s in segs], wins, 0)
+    psi = _assemble_1d([s.PSI.cpu().numpy() for s in segs], wins, 1)
+    a, b = segs[0].A.cpu().numpy(), segs[0].B.cpu().numpy()
+    for s in segs:
+        s.close()
+    return _solution_1d(X, Y, config, phi, psi, a, b, it, conv, status, hist, abs_its, 0.0)
