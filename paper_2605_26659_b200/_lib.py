@@ -14,6 +14,8 @@ from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfinom_b200.so")
+if os.environ.get("FINOM_LIB"):  # (A/B timing of a library variant built in-tree)
+    LIB_PATH = os.path.abspath(os.environ["FINOM_LIB"])
 
 _c_i64 = ctypes.c_int64
 _c_dbl = ctypes.c_double
