@@ -308,21 +308,25 @@ class BatchSolver1D:
 
 
 def _pipeline_ranges(sizes):
-    """Problem ranges of the batched API's pipeline stages: >= 1024 problems
-    and >= 2^22 points per stage, at most 8 stages, one stage for small
-    batches.  FINOM_PIPE_STAGES overrides the stage count.  (Config 5, 8192 x
-    16384, warm calls: 1 stage 1.53 s, 4: 1.22-1.25, 6: 1.20-1.24, 8: 1.25,
-    12: 1.30.  A stage's own loop needs enough problems to fill the GPU
-    evenly -- 1024 problems of g = 16 warps are 7 rounds of the 2368 resident
-    warps at 99 % occupancy, 256 would leave 14 % idle -- so a rank of an
-    8-way split (1024 problems) runs one stage.)"""
+    """Problem ranges of the batched API's pipeline stages: k = P // 2048
+    stages (at most 8) of >= 2048 problems and >= 2^22 points, one stage for
+    smaller batches; with FINOM_PIPE_FIRST set, a small first stage of that
+    many problems (the device starts sooner) before the k stages.
+    FINOM_PIPE_STAGES overrides k.  (Config 5, 8192 x 16384, warm calls: 1
+    stage 1.53 s; 8 stages of 1024 1.23-1.81 s -- each stage's loop takes 144
+    ms against 131 for 1/8 of the batch, and the host's preparation of a
+    1024-problem stage sometimes outlasts it; 4 stages of 2048 1.20-1.21 s,
+    each loop 265-279 ms.)"""
     P, pts = len(sizes), int(np.sum(sizes))
-    k = min(8, P // 1024, pts >> 22)
+    k = min(8, P // 2048, pts >> 22)
     env = os.environ.get("FINOM_PIPE_STAGES")
     if env:
         k = int(env)
     k = max(1, min(k, P))
-    return [(P * i // k, P * (i + 1) // k) for i in range(k)]
+    f = int(os.environ.get("FINOM_PIPE_FIRST", "0")) if k > 1 else 0
+    f = max(0, min(f, P - k))
+    return ([(0, f)] if f else []) + [(f + (P - f) * i // k, f + (P - f) * (i + 1) // k)
+                                      for i in range(k)]
 
 
 def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
@@ -377,6 +381,7 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
             _lib.stage_copy(1, h, d)
 
     pending = None
+    marks = []
     stages = []  # (kept to the end: destroying a plan waits for every stream it ran on)
     for lo, hi in _pipeline_ranges(nx):
         ts = perf_counter()
@@ -394,10 +399,14 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
         comp.wait_event(ready)
         for t in (bs.u, bs.v, bs.phi, bs.psi, bs.a, bs.b, bs.cost, bs.hist, bs.info, bs.abs_its):
             t.record_stream(comp)
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(comp)
         bs.solve(itr, config.tol, config.stabilize, config.absorb_threshold, sync=False)
         bs.compute_cost()
-        done = torch.cuda.Event()
+        done = torch.cuda.Event(enable_timing=True)
         done.record(comp)
+        if verbose:
+            marks.append((start, done))
         tq = perf_counter()
         if pending is not None:
             fetch(pending)
@@ -413,8 +422,12 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
     sols = BatchSolutions(xs, ys, xoff, yoff, np.array(eps), config, info, cost,
                           phi, psi, a, b, hist, abs_its, wall, setup[0])
     if verbose:
-        print("sinkhorn_1d_batched: %d stage(s), setup %.1f ms, call %.1f ms" % (
-            len(_pipeline_ranges(nx)), 1e3 * setup[0], 1e3 * wall), flush=True)
+        print("sinkhorn_1d_batched: %d stage(s), setup %.1f ms, call %.1f ms; device loop "
+              "+ cost per stage %s ms, gaps %s ms" % (
+                  len(_pipeline_ranges(nx)), 1e3 * setup[0], 1e3 * wall,
+                  ["%.1f" % a.elapsed_time(b) for a, b in marks],
+                  ["%.1f" % marks[k][1].elapsed_time(marks[k + 1][0])
+                   for k in range(len(marks) - 1)]), flush=True)
     return sols
 
 

@@ -21,8 +21,8 @@ def _batch(B, n):
 def test_stage_ranges():
     sizes = np.full(8192, 16384)
     r = S._pipeline_ranges(sizes)
-    assert len(r) == 8 and r[0] == (0, 1024) and r[-1] == (7168, 8192)
-    assert len(S._pipeline_ranges(np.full(1024, 16384))) == 1  # (a rank of an 8-way split)
+    assert len(r) == 4 and r[0] == (0, 2048) and r[-1] == (6144, 8192)
+    assert len(S._pipeline_ranges(np.full(2048, 16384))) == 1  # (a rank of a 4-way split)
     assert S._pipeline_ranges(np.full(40, 1000)) == [(0, 40)]
 
 
