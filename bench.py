@@ -431,7 +431,7 @@ def main():
     ms_max = float(ms_t.item())
     value = pts_all * itr * args.steps / (ms_max * 1e-3)
 
-    lib = _lib.load()
+    lib = bs.plan.lib  # (the 512-element-tile build for config 2, lib_for)
     group = int(lib.finom_solve1d_group(bs.plan.handle))
     NX, NY = bs.u.numel(), bs.v.numel()
     # algorithmic bytes: per iteration 40n + 48m unabsorbed,
@@ -459,7 +459,7 @@ def main():
         _lib.check(lib.finom_profile1d(bs.plan.handle, _lib.ptr(bs.u), _lib.ptr(bs.v),
                                        _lib.ptr(bs.phi), _lib.ptr(bs.psi), _lib.ptr(bs.a),
                                        _lib.ptr(bs.b), itr, 1, 200.0, _lib.ptr(hist_dev),
-                                       _lib.ptr(prof), _lib.stream_ptr()), "finom_profile1d")
+                                       _lib.ptr(prof), _lib.stream_ptr()), "finom_profile1d", lib)
         t_it = (prof[0] + prof[1]) * 1e-3
         kernel = "k_step<A>+k_resolve<A>+k_step<B>+k_resolve<B>"
         traffic_key = "k_step"

@@ -14,6 +14,13 @@ from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfinom_b200.so")
+# The same sources built with 512-element tiles (16 merged elements per lane,
+# 8 warps per SM): the tile-parallel loop of a few large problems runs faster
+# on it (config 2: 2.19e10 vs 2.03e10 pts*it/s -- half the tiles, half the
+# per-tile carry, record and reduction work), the group solve of batches and
+# small problems on the 256-element tiles (config 5: 1040 vs 1209 ms per
+# solve; config 1: 32.3 vs 33.5 us per iteration).  See lib_for().
+LIB_T512_PATH = os.path.join(_HERE, "libfinom_b200_t512.so")
 if os.environ.get("FINOM_LIB"):  # (A/B timing of a library variant built in-tree)
     LIB_PATH = os.path.abspath(os.environ["FINOM_LIB"])
 
@@ -100,17 +107,46 @@ def load(require_device=True):
         if not os.path.exists(LIB_PATH):
             raise DeviceError(
                 "CUDA extension %s is not built; run __graft_entry__.build()" % LIB_PATH)
-        lib = ctypes.CDLL(LIB_PATH)
-        for name, (res, args) in SIGNATURES.items():
-            fn = getattr(lib, name)
-            fn.restype = res
-            fn.argtypes = args
-        _lib = lib
+        _lib = _bind(ctypes.CDLL(LIB_PATH))
     if require_device:
         import torch
         if not torch.cuda.is_available():
             raise DeviceError("no CUDA device visible; the FINOM B200 path has no CPU fallback")
     return _lib
+
+
+_lib_t512 = None
+
+
+def _bind(lib):
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def use_t512(P, merged):
+    """lib_for's rule (host only)."""
+    want = os.environ.get("FINOM_TILE")
+    return want == "512" or (want != "256" and P <= 4 and merged >= (1 << 20))
+
+
+def lib_for(P, merged):
+    """The library a plan of P problems with `merged` elements (sum of n + m)
+    runs on: the 512-element-tile build for at most 4 problems of >= 2^20
+    merged elements (the tile-parallel loop over the whole GPU), the default
+    256-element build otherwise.  FINOM_TILE=256 / 512 forces one."""
+    global _lib_t512
+    if not use_t512(P, merged) or os.environ.get("FINOM_LIB"):
+        return load()
+    if _lib_t512 is None:
+        load()  # (device check)
+        if not os.path.exists(LIB_T512_PATH):
+            raise DeviceError("CUDA extension %s is not built; run __graft_entry__.build()"
+                              % LIB_T512_PATH)
+        _lib_t512 = _bind(ctypes.CDLL(LIB_T512_PATH))
+    return _lib_t512
 
 
 def stage_copy(direction, host, dev):
@@ -162,10 +198,12 @@ def stream_ptr():
     return torch.cuda.current_stream().cuda_stream
 
 
-def check(code, what):
-    """Map a C status >= 100 to DeviceError; return FINOM status 0/1/2."""
+def check(code, what, lib=None):
+    """Map a C status >= 100 to DeviceError; return FINOM status 0/1/2.
+    (lib: the library the call went to, for its error message.)"""
     if code >= 100:
-        raise DeviceError("%s failed: %s" % (what, last_error()))
+        msg = (lib or load(False)).finom_last_error().decode()
+        raise DeviceError("%s failed: %s" % (what, msg))
     return code
 
 
@@ -173,9 +211,9 @@ class Plan1D:
     """Device plan for a batch of P 1D problems (finom_plan1d_create)."""
 
     def __init__(self, xs, ys, eps):
-        lib = load()
         xs = [np.ascontiguousarray(x, dtype=np.float64) for x in xs]
         ys = [np.ascontiguousarray(y, dtype=np.float64) for y in ys]
+        lib = lib_for(len(xs), sum(x.size for x in xs) + sum(y.size for y in ys))
         self.P = len(xs)
         self.xoff = np.zeros(self.P + 1, dtype=np.int64)
         self.yoff = np.zeros(self.P + 1, dtype=np.int64)
@@ -187,7 +225,7 @@ class Plan1D:
         if self.P == 1:
             check(lib.finom_plan1d_create(1, ptr(self.xoff), ptr(xs[0]), ptr(self.yoff),
                                           ptr(ys[0]), ptr(self.eps), stream_ptr(),
-                                          ctypes.byref(h)), "finom_plan1d_create")
+                                          ctypes.byref(h)), "finom_plan1d_create", lib)
         else:  # per-problem arrays staged as they are (no host concatenation)
             n = np.diff(self.xoff)
             m = np.diff(self.yoff)
@@ -195,7 +233,7 @@ class Plan1D:
             yp = np.array([y.ctypes.data for y in ys], dtype=np.uint64)
             check(lib.finom_plan1d_create_v(self.P, ptr(n), ptr(xp), ptr(m), ptr(yp),
                                             ptr(self.eps), stream_ptr(), ctypes.byref(h)),
-                  "finom_plan1d_create_v")
+                  "finom_plan1d_create_v", lib)
         self._h = h
         self._lib = lib
 
@@ -203,9 +241,14 @@ class Plan1D:
     def handle(self):
         return self._h
 
+    @property
+    def lib(self):
+        """The library the plan lives in (every call on the handle goes there)."""
+        return self._lib
+
     def info(self):
         out = np.zeros(8, dtype=np.int64)
-        check(self._lib.finom_plan1d_info(self._h, ptr(out)), "finom_plan1d_info")
+        check(self._lib.finom_plan1d_info(self._h, ptr(out)), "finom_plan1d_info", self._lib)
         keys = ("P", "tiles", "NX", "NY", "max_tiles", "tile", "threads", "smem")
         return dict(zip(keys, (int(v) for v in out)))
 

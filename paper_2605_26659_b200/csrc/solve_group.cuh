@@ -22,7 +22,10 @@
 
 namespace fb {
 
-constexpr int GW = 16;                  // warps per CTA
+#ifndef FB_GW
+#define FB_GW 16
+#endif
+constexpr int GW = FB_GW;               // warps per CTA
 constexpr int GTHR = 32 * GW;
 constexpr int WREG = WST > WSM ? WST : WSM;  // shared doubles per warp (step / absorb)
 

@@ -34,6 +34,8 @@
 
 namespace fb {
 
+constexpr int SQE = 8;                 // points per lane of a square-sweep tile
+
 // Partials of the 2D scaling update (k_epi2d, fused square sweeps).
 struct EpiPart {
   double err, vmax, vmin;
@@ -66,9 +68,9 @@ __device__ __forceinline__ void epi_block_part(double err, double vmax, double v
   }
 }
 
-constexpr int SQT = 32 * EPT;          // points per tile
-constexpr int SQF = 2 * EPT * 32;      // double2 of F per tile
-constexpr int SQW = EPT * 32;          // double2 of W per tile
+constexpr int SQT = 32 * SQE;          // points per tile
+constexpr int SQF = 2 * SQE * 32;      // double2 of F per tile
+constexpr int SQW = SQE * 32;          // double2 of W per tile
 
 struct SqArgs {
   const double *Z;        // the line mesh (z[0..n))
@@ -115,14 +117,14 @@ __global__ void __launch_bounds__(NTHR) k_sq_build(SqArgs a) {
   const double *be = a.beta ? a.beta + (size_t)p * a.n : nullptr;
   auto A = [&](int r) { return al ? al[r] : 0.0; };
   auto B = [&](int r) { return be ? be[r] : 0.0; };
-  const int r0 = t * SQT + EPT * lane;
+  const int r0 = t * SQT + SQE * lane;
   // exponent argument: baked tables divide by eps (kernel1d.py:142, :148;
   // q_div is the IEEE quotient), the dyn form multiplies by inv_eps
   // (_kernels.py:140-159)
   auto arg = [&](double num) { return a.baked ? q_div(num, a.eps, a.inv) : __dmul_rn(num, a.inv); };
-  double rho[EPT], del[EPT], sig[EPT], mu[EPT];
+  double rho[SQE], del[SQE], sig[SQE], mu[SQE];
 #pragma unroll
-  for (int k = 0; k < EPT; ++k) {
+  for (int k = 0; k < SQE; ++k) {
     const int r = r0 + k;
     rho[k] = 1.0; del[k] = 0.0; sig[k] = 1.0; mu[k] = 0.0;  // padding: identity steps
     if (r < a.n) {
@@ -137,12 +139,12 @@ __global__ void __launch_bounds__(NTHR) k_sq_build(SqArgs a) {
     }
   }
   // in-lane suffix products of rho (after k) and prefix products of sigma (before k)
-  double sp[EPT], pp[EPT];
-  sp[EPT - 1] = 1.0;
-  for (int k = EPT - 2; k >= 0; --k) sp[k] = __dmul_rn(rho[k + 1], sp[k + 1]);
+  double sp[SQE], pp[SQE];
+  sp[SQE - 1] = 1.0;
+  for (int k = SQE - 2; k >= 0; --k) sp[k] = __dmul_rn(rho[k + 1], sp[k + 1]);
   pp[0] = 1.0;
-  for (int k = 1; k < EPT; ++k) pp[k] = __dmul_rn(sig[k - 1], pp[k - 1]);
-  const double rt = __dmul_rn(rho[0], sp[0]), st = __dmul_rn(sig[EPT - 1], pp[EPT - 1]);
+  for (int k = 1; k < SQE; ++k) pp[k] = __dmul_rn(sig[k - 1], pp[k - 1]);
+  const double rt = __dmul_rn(rho[0], sp[0]), st = __dmul_rn(sig[SQE - 1], pp[SQE - 1]);
   // across lanes: products of later lanes' rho, of earlier lanes' sigma
   double sx = rt, px = st;
 #pragma unroll
@@ -159,9 +161,9 @@ __global__ void __launch_bounds__(NTHR) k_sq_build(SqArgs a) {
   const size_t tile = (size_t)p * a.tl + t;
   double2 *F = a.F + tile * SQF, *W = a.W + tile * SQW;
 #pragma unroll
-  for (int k = 0; k < EPT; ++k) {
+  for (int k = 0; k < SQE; ++k) {
     F[k * 32 + lane] = make_double2(rho[k], del[k]);
-    F[(EPT + k) * 32 + lane] = make_double2(sig[k], mu[k]);
+    F[(SQE + k) * 32 + lane] = make_double2(sig[k], mu[k]);
     W[k * 32 + lane] = a.wraw ? make_double2(__dmul_rn(sp[k], sxe), __dmul_rn(pp[k], pxe))
                               : make_double2(__dmul_rn(del[k], __dmul_rn(sp[k], sxe)),
                                              __dmul_rn(mu[k], __dmul_rn(pp[k], pxe)));
@@ -178,10 +180,10 @@ __global__ void __launch_bounds__(NTHR) k_sq_build_d(SqArgs a) {
   if (w >= (long long)a.lines * a.tl) return;
   const int p = (int)(w / a.tl), t = (int)(w % a.tl);
   const double *be = a.beta + (size_t)p * a.n;
-  const int r0 = t * SQT + EPT * lane;
+  const int r0 = t * SQT + SQE * lane;
   double2 *D = a.D + (size_t)w * SQW;
 #pragma unroll
-  for (int k = 0; k < EPT; ++k) {
+  for (int k = 0; k < SQE; ++k) {
     const int r = r0 + k;
     double del = 0.0, mu = 0.0;
     if (r < a.n) {
@@ -193,25 +195,25 @@ __global__ void __launch_bounds__(NTHR) k_sq_build_d(SqArgs a) {
   }
 }
 
-// This lane's v_r for r = t0 + EPT lane .. + EPT (EPT + 1 values, zero past
+// This lane's v_r for r = t0 + SQE lane .. + SQE (SQE + 1 values, zero past
 // the line): the warp's SQT + 1 values are loaded coalesced into xs (one pad
-// double per EPT, so the lanes' EPT-strided reads hit distinct banks), then
+// double per SQE, so the lanes' SQE-strided reads hit distinct banks), then
 // each lane reads its run.  (A lane reading its run straight from global
 // memory touches 32 sectors per instruction.)
-constexpr int SQX = SQT + SQT / EPT + 2;  // staging doubles per warp
-__device__ __forceinline__ int sq_pad(int i) { return i + i / EPT; }
+constexpr int SQX = SQT + SQT / SQE + 2;  // staging doubles per warp
+__device__ __forceinline__ int sq_pad(int i) { return i + i / SQE; }
 __device__ __forceinline__ void sq_load_v(const double *v, int t0, int n, double *xs,
-                                          double (&x)[EPT + 1]) {
+                                          double (&x)[SQE + 1]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int k = 0; k < EPT; ++k) {
+  for (int k = 0; k < SQE; ++k) {
     const int i = lane + 32 * k;
     xs[sq_pad(i)] = t0 + i < n ? __ldg(v + t0 + i) : 0.0;
   }
   if (lane == 0) xs[sq_pad(SQT)] = t0 + SQT < n ? __ldg(v + t0 + SQT) : 0.0;
   __syncwarp();
 #pragma unroll
-  for (int k = 0; k <= EPT; ++k) x[k] = xs[sq_pad(EPT * lane + k)];
+  for (int k = 0; k <= SQE; ++k) x[k] = xs[sq_pad(SQE * lane + k)];
   __syncwarp();
 }
 
@@ -228,11 +230,11 @@ __global__ void __launch_bounds__(NTHR) k_sq_pre(SqArgs a) {
   const double2 *W = a.W + rec * SQW;
   const double2 *D = a.D ? a.D + (size_t)w * SQW : nullptr;
   __shared__ double xs[WPC][SQX];
-  double x[EPT + 1];
+  double x[SQE + 1];
   sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, xs[threadIdx.x >> 5], x);
   double cf = 0.0, cb = 0.0;
 #pragma unroll
-  for (int k = 0; k < EPT; ++k) {
+  for (int k = 0; k < SQE; ++k) {
     double2 wk = __ldg(W + k * 32 + lane);
     if (D) {  // split records: the same products as k_sq_build's W
       const double2 dk = __ldcs(D + k * 32 + lane);
@@ -338,23 +340,23 @@ __global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
     const size_t tile = (size_t)p * a.tl + t;
     const size_t rec = a.shared || a.D ? (size_t)t : tile;
     const double2 *F = a.F + rec * SQF;
-    double2 f0[EPT], f1[EPT];
+    double2 f0[SQE], f1[SQE];
     if (a.D) {  // split records: shared ratios, the line's (delta, mu)
       const double2 *D = a.D + tile * SQW;
 #pragma unroll
-      for (int k = 0; k < EPT; ++k) {
+      for (int k = 0; k < SQE; ++k) {
         const double2 dk = __ldcs(D + k * 32 + lane);
         f0[k] = make_double2(__ldg(&F[k * 32 + lane].x), dk.x);
-        f1[k] = make_double2(__ldg(&F[(EPT + k) * 32 + lane].x), dk.y);
+        f1[k] = make_double2(__ldg(&F[(SQE + k) * 32 + lane].x), dk.y);
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < EPT; ++k) {
+      for (int k = 0; k < SQE; ++k) {
         f0[k] = __ldcs(F + k * 32 + lane);
-        f1[k] = __ldcs(F + (EPT + k) * 32 + lane);
+        f1[k] = __ldcs(F + (SQE + k) * 32 + lane);
       }
     }
-    double x[EPT + 1];
+    double x[SQE + 1];
     sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, so[warp], x);
     double pin = 0.0, qin = 0.0;  // the tile's incoming P (lane 0) / Q (lane 31)
     // (the tile's exclusive maps applied to the line's incoming states: zero,
@@ -370,14 +372,14 @@ __global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
     // lane maps: forward P_end = af P_in + cf, backward Q_first = ab Q_after + cb
     double af = 1.0, cf = 0.0, ab = 1.0, cb = 0.0;
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
+    for (int k = 0; k < SQE; ++k) {
       f0[k].y = __dmul_rn(f0[k].y, x[k]);      // delta v
       f1[k].y = __dmul_rn(f1[k].y, x[k + 1]);  // mu v_{+1}
       af = __dmul_rn(f0[k].x, af);
       cf = __dadd_rn(__dmul_rn(f0[k].x, cf), f0[k].y);
     }
 #pragma unroll
-    for (int k = EPT - 1; k >= 0; --k) {
+    for (int k = SQE - 1; k >= 0; --k) {
       ab = __dmul_rn(f1[k].x, ab);
       cb = __dadd_rn(__dmul_rn(f1[k].x, cb), f1[k].y);
     }
@@ -398,14 +400,14 @@ __global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
     if (lane == 31) qq = qin;
     // final recurrences (_kernels.py:65-67 / :80-87 order)
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
+    for (int k = 0; k < SQE; ++k) {
       pp = __dadd_rn(__dmul_rn(f0[k].x, pp), f0[k].y);
       f0[k].y = pp;
     }
 #pragma unroll
-    for (int k = EPT - 1; k >= 0; --k) {
+    for (int k = SQE - 1; k >= 0; --k) {
       qq = __dadd_rn(__dmul_rn(f1[k].x, qq), f1[k].y);
-      so[warp][EPT * lane + k] = __dadd_rn(f0[k].y, qq);
+      so[warp][SQE * lane + k] = __dadd_rn(f0[k].y, qq);
     }
   }
   __syncthreads();

@@ -136,10 +136,10 @@ def _run(op, vec, mode):
     if op.absorbed:
         a = torch.from_numpy(np.ascontiguousarray(op.absorption_left)).to(dev)
         b = torch.from_numpy(np.ascontiguousarray(op.absorption_right)).to(dev)
-    lib = _lib.load()
+    lib = plan.lib
     _lib.check(lib.finom_apply1d(plan.handle, _lib.ptr(a), _lib.ptr(b), _lib.ptr(tin), mode,
                                  _lib.ptr(out), _lib.ptr(out2), _lib.stream_ptr()),
-               "finom_apply1d")
+               "finom_apply1d", lib)
     if mode == 2:
         return out.cpu().numpy(), out2.cpu().numpy()
     return out.cpu().numpy()

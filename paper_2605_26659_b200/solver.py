@@ -195,10 +195,10 @@ class GpuAdapter1D:
             ta = torch.from_numpy(np.ascontiguousarray(self.a)).to(dev)
             tb = torch.from_numpy(np.ascontiguousarray(self.b)).to(dev)
         res = torch.zeros(6, dtype=torch.float64, device=dev)
-        lib = _lib.load()
+        lib = plan.lib
         _lib.check(lib.finom_iterate1d(plan.handle, _lib.ptr(tu), _lib.ptr(tv), _lib.ptr(tphi),
                                        _lib.ptr(tpsi), _lib.ptr(ta), _lib.ptr(tb), _lib.ptr(res),
-                                       _lib.stream_ptr()), "finom_iterate1d")
+                                       _lib.stream_ptr()), "finom_iterate1d", lib)
         r = res.cpu().numpy()
         phi[:] = tphi.cpu().numpy()
         psi[:] = tpsi.cpu().numpy()
@@ -214,8 +214,8 @@ def sinkhorn_1d(x, y, u, v, config):
         raise DimensionMismatch("u must have one weight per source node")
     if len(v.weights) != len(y):
         raise DimensionMismatch("v must have one weight per target node")
-    lib = _lib.load()
     n, m, itr = len(x), len(y), int(config.itr_max)
+    lib = _lib.lib_for(1, n + m)
     phi, a = np.empty(n), np.empty(n)
     psi, b = np.empty(m), np.empty(m)
     hist = np.zeros(itr)
@@ -228,7 +228,7 @@ def sinkhorn_1d(x, y, u, v, config):
         config.epsilon, itr, float(config.tol), int(bool(config.stabilize)),
         float(config.absorb_threshold), _lib.ptr(phi), _lib.ptr(psi), _lib.ptr(a), _lib.ptr(b),
         _lib.ptr(hist), _lib.ptr(info), _lib.ptr(abs_its), _lib.ptr(cost), _lib.ptr(timing)),
-        "finom_sinkhorn1d_host")
+        "finom_sinkhorn1d_host", lib)
     raise_status(status)
     its, conv = int(info[0]), bool(info[1])
     op = kernel1d.build_operator(x, y, config.epsilon)
@@ -291,19 +291,19 @@ class BatchSolver1D:
         (0/1/2) -- or, with sync=False, 0 as soon as the loop is queued (the
         per-problem status is then info[5 p + 2] once the stream has run)."""
         self._bufs(int(itr_max))
-        lib = _lib.load()
+        lib = self.plan.lib
         fn = lib.finom_solve1d if sync else lib.finom_solve1d_async
         return _lib.check(fn(
             self.plan.handle, _lib.ptr(self.u), _lib.ptr(self.v), _lib.ptr(self.phi),
             _lib.ptr(self.psi), _lib.ptr(self.a), _lib.ptr(self.b), int(itr_max), float(tol),
             int(bool(stabilize)), float(absorb_threshold), _lib.ptr(self.hist),
-            _lib.ptr(self.info), _lib.ptr(self.abs_its), _lib.stream_ptr()), "finom_solve1d")
+            _lib.ptr(self.info), _lib.ptr(self.abs_its), _lib.stream_ptr()), "finom_solve1d", lib)
 
     def compute_cost(self):
-        lib = _lib.load()
+        lib = self.plan.lib
         _lib.check(lib.finom_cost1d(self.plan.handle, _lib.ptr(self.a), _lib.ptr(self.b),
                                     _lib.ptr(self.phi), _lib.ptr(self.psi),
-                                    _lib.ptr(self.cost), _lib.stream_ptr()), "finom_cost1d")
+                                    _lib.ptr(self.cost), _lib.stream_ptr()), "finom_cost1d", lib)
         return self.cost
 
 
@@ -524,7 +524,8 @@ def transport_cost_fast(solution):
     ta = t(op.absorption_left) if op.absorbed else None
     tb = t(op.absorption_right) if op.absorbed else None
     out = torch.zeros(1, dtype=torch.float64, device=dev)
-    lib = _lib.load()
+    lib = plan.lib
     _lib.check(lib.finom_cost1d(plan.handle, _lib.ptr(ta), _lib.ptr(tb), _lib.ptr(tphi),
-                                _lib.ptr(tpsi), _lib.ptr(out), _lib.stream_ptr()), "finom_cost1d")
+                                _lib.ptr(tpsi), _lib.ptr(out), _lib.stream_ptr()), "finom_cost1d",
+               lib)
     return float(out.item())

@@ -27,11 +27,31 @@ def test_header_declares_entry_points():
 
 
 def test_library_exports_every_declared_symbol():
+    import ctypes
     from paper_2605_26659_b200 import _lib
     lib = _lib.load(require_device=False)
+    t512 = ctypes.CDLL(_lib.LIB_T512_PATH)  # (the 512-element-tile build, _lib.lib_for)
     for name in declared():
+        if name == "finom_phase_read":  # (debug builds only)
+            continue
         assert hasattr(lib, name), name
+        assert hasattr(t512, name), name
     assert set(_lib.SIGNATURES) >= set(declared()) - {"finom_phase_read"}
+    t512.finom_build_info.restype = ctypes.c_char_p
+    assert b"TILE=512" in t512.finom_build_info()
+    assert "TILE=256" in lib.finom_build_info().decode()
+
+
+def test_library_selection_rule(monkeypatch):
+    from paper_2605_26659_b200 import _lib
+    monkeypatch.delenv("FINOM_TILE", raising=False)
+    assert _lib.use_t512(1, 2 * (1 << 22))        # config 2
+    assert not _lib.use_t512(1, 20_000)           # config 1
+    assert not _lib.use_t512(8192, 8192 * 32768)  # config 5 (the group solve)
+    monkeypatch.setenv("FINOM_TILE", "512")
+    assert _lib.use_t512(1, 20_000)
+    monkeypatch.setenv("FINOM_TILE", "256")
+    assert not _lib.use_t512(1, 2 * (1 << 22))
 
 
 def test_library_is_sm100a():
