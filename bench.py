@@ -242,7 +242,9 @@ def run_2d(args, cfg, wl, world=1, rank=0):
                 "CUDA events around K device-resident solves (GridSolver2D / finom_solve2d: "
                 "device-looped CUDA graph, host sync only at absorptions)")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": psrc,
+                     "frac": achieved / peak, "traffic": ncu_traffic("iteration", cfg),
+                     "traffic_unit": "DRAM bytes per iteration (ncu launch list)",
+                     "peak_source": psrc,
                      "kernel": "whole iteration: 4 line sweeps (k_sq_pre/k_sq_scan/k_sq_apply) "
                                "+ fused scaling updates",
                      "algorithmic_bytes_per_solve": abytes,
