@@ -27,7 +27,37 @@ namespace fb {
 #endif
 constexpr int GW = FB_GW;               // warps per CTA
 constexpr int GTHR = 32 * GW;
-constexpr int WREG = WST > WSM ? WST : WSM;  // shared doubles per warp (step / absorb)
+// The next half's tile maps of a warp's first STASH tiles stay in shared
+// memory after the loop's working area (the carries then need no global
+// round trip: the node loads took 5.4 of a half's 11 us of carries at config 5,
+// their lines long evicted from L2); absorb_core's larger area overlaps the
+// stash, so a rebuild invalidates it.
+constexpr int STASH = 16;
+constexpr int WSTASH = WST + 2 * 5 * STASH;
+constexpr int WREG = WSTASH > WSM ? WSTASH : WSM;  // shared doubles per warp (step / absorb)
+
+#ifdef FB_DBG_GRP
+// (timing experiment: globaltimer stamps of one iteration's phases by warp 0
+// of problem 0, read by finom_grp_read; tools/grp_time.py)
+__device__ unsigned long long g_grp[16];
+__device__ int g_grp_on;
+__device__ __forceinline__ void grp_stamp(int k) {
+  unsigned long long t_;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+  g_grp[k] = t_;
+}
+#define GRP_STAMP(k)                                                    \
+  do {                                                                  \
+    if (prob == 0 && j == 0 && lane == 0 && it == 20) grp_stamp(k);     \
+  } while (0)
+#define GRP_STAMP_IN(k)                                                 \
+  do {                                                                  \
+    if (g_grp_on == (int)(blockIdx.x * 32 + (threadIdx.x >> 5)) + 1 && lane == 0) grp_stamp(k); \
+  } while (0)
+#else
+#define GRP_STAMP(k)
+#define GRP_STAMP_IN(k)
+#endif
 
 struct GX;
 struct GroupArgs {
@@ -127,7 +157,7 @@ __device__ __forceinline__ void group_prefix(const Grp &G, int lane, double &p, 
 // epilogue or by the table build), forward composed left to right, backward
 // right to left; guarded compositions (a structural zero stays zero).
 __device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, int e,
-                                           const Grp &G, int lane) {
+                                           const Grp &G, int lane, const Tf *stash) {
   const int g = G.g, j = G.j;
   GX *gx = G.gx;
   const Node *nd = R.lev[0];
@@ -135,10 +165,19 @@ __device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, 
   const int L = (n + 31) / 32;
   const int lb = min(b + lane * L, e), le = min(lb + L, e);
   Tf f = tf_id(), bk = tf_id();
-  for (int t = lb; t < le; ++t) f = tf_cat_g(f, ldcg_tf(&nd[t].tf));
-  for (int t = le - 1; t >= lb; --t) bk = tf_cat_g(bk, ldcg_tf(&nd[t].tb));
+  if (stash && n <= STASH) {  // (L <= 1: this lane's tile, if any)
+    if (lb < le) {
+      f = stash[2 * (lb - b)];
+      bk = stash[2 * (lb - b) + 1];
+    }
+  } else {
+    for (int t = lb; t < le; ++t) f = tf_cat_g(f, ldcg_tf(&nd[t].tf));
+    for (int t = le - 1; t >= lb; --t) bk = tf_cat_g(bk, ldcg_tf(&nd[t].tb));
+  }
+  GRP_STAMP_IN(8);
   Tf xf, xb, totf, totb;
   warp_scan2<true>(f, bk, xf, xb, totf, totb);
+  GRP_STAMP_IN(9);
   double p = 0.0, acc = 0.0, q = 0.0, accb = 0.0;
   if (g > 1) {
     if (lane == 0) {
@@ -146,6 +185,7 @@ __device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, 
       gx[j].b = totb;
     }
     G.sync();
+    GRP_STAMP_IN(10);
     // the totals of the group's earlier warps (forward) and later warps
     // (backward), applied to the problem's zero boundary states
     if (g <= 16) {
@@ -154,20 +194,30 @@ __device__ __noinline__ void group_carries(const Resolve &R, double *S4, int b, 
     } else {
       group_prefix(G, lane, p, acc, q, accb);
     }
+    GRP_STAMP_IN(11);
     // (no barrier: the partials write other fields of gx, and the next
     // writes of f / b come after the partials' barrier)
   }
   tf_apply_g(xf, p, acc);
   tf_apply_g(xb, q, accb);
-  for (int t = lb; t < le; ++t) {
-    S4[4 * (size_t)t] = p;
-    S4[4 * (size_t)t + 1] = acc;
-    tf_apply_g(ldcg_tf(&nd[t].tf), p, acc);
-  }
-  for (int t = le - 1; t >= lb; --t) {
-    S4[4 * (size_t)t + 2] = q;
-    S4[4 * (size_t)t + 3] = accb;
-    tf_apply_g(ldcg_tf(&nd[t].tb), q, accb);
+  if (stash && n <= STASH) {
+    if (lb < le) {
+      S4[4 * (size_t)lb] = p;
+      S4[4 * (size_t)lb + 1] = acc;
+      S4[4 * (size_t)lb + 2] = q;
+      S4[4 * (size_t)lb + 3] = accb;
+    }
+  } else {
+    for (int t = lb; t < le; ++t) {
+      S4[4 * (size_t)t] = p;
+      S4[4 * (size_t)t + 1] = acc;
+      tf_apply_g(ldcg_tf(&nd[t].tf), p, acc);
+    }
+    for (int t = le - 1; t >= lb; --t) {
+      S4[4 * (size_t)t + 2] = q;
+      S4[4 * (size_t)t + 3] = accb;
+      tf_apply_g(ldcg_tf(&nd[t].tb), q, accb);
+    }
   }
   __syncwarp();
 }
@@ -205,7 +255,7 @@ template <int HALF>
 __device__ __forceinline__ void group_tile(const Dev &d, int t, const TileStep &ts, bool next,
                                            const TileStep &nts, double *wsm,
                                            unsigned long long *bar, int lane, unsigned &phase,
-                                           const double *init, double *part) {
+                                           const double *init, double *part, Tf *stash) {
   TileIn in;
   in.t = t;
   in.nr = HALF == 0 ? ts.ny : ts.nx;
@@ -242,9 +292,10 @@ __device__ __forceinline__ void group_tile(const Dev &d, int t, const TileStep &
   __syncwarp();
 #ifdef FB_DBG_PHASE
   long long ph_t0 = 0;
-  tile_compute<HALF, true, false>(d, in, tf_id(), lane, ph_t0, nullptr, part, true, st0, st1);
+  tile_compute<HALF, true, false>(d, in, tf_id(), lane, ph_t0, nullptr, part, true, st0, st1,
+                                  stash);
 #else
-  tile_compute<HALF, true, false>(d, in, tf_id(), lane, nullptr, part, true, st0, st1);
+  tile_compute<HALF, true, false>(d, in, tf_id(), lane, nullptr, part, true, st0, st1, stash);
 #endif
 }
 
@@ -374,17 +425,30 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
     G.sync();
     int it = 0, status = 0, fail_it = 0, sbuf = 0, n_abs = 0, converged = 0;
     bool absorbed = false;
+    bool stash_ok = false;  // (group_build wrote half A's maps to global only)
+    Tf *stash = reinterpret_cast<Tf *>(wsm + WST);
     double err = 0.0;
     for (;;) {
       // ---- half A: psi <- v / K'^T phi (_kernels.py:278-314)
+#ifdef FB_DBG_GRP
+      if (prob == 0 && j == 0 && lane == 0)
+        g_grp_on = it == 20 ? (int)(blockIdx.x * 32 + (threadIdx.x >> 5)) + 1 : 0;
+#endif
+      GRP_STAMP(0);
       proxy_fence();
-      group_carries(d.RA, a.S4, b, e, G, lane);
+      group_carries(d.RA, a.S4, b, e, G, lane, stash_ok ? stash : nullptr);
+      stash_ok = true;  // (half A's tiles write it for half B)
+#ifdef FB_DBG_GRP
+      if (prob == 0 && j == 0 && lane == 0) g_grp_on = 0;
+#endif
+      GRP_STAMP(1);
       double pw[4] = {0.0, 0.0, INFINITY, -1.0};
       TileStep ts = d.steps[b < e ? b : 0];
       for (int t = b; t < e; ++t) {
         double pt[4];
         const TileStep nts = d.steps[t + 1 < e ? t + 1 : t];
-        group_tile<0>(d, t, ts, t + 1 < e, nts, wsm, mb, lane, phase, a.S4 + 4 * (size_t)t, pt);
+        group_tile<0>(d, t, ts, t + 1 < e, nts, wsm, mb, lane, phase, a.S4 + 4 * (size_t)t, pt,
+                      t - b < STASH ? stash + 2 * (t - b) : nullptr);
         ts = nts;
         pw[0] = __dadd_rn(pw[0], pt[0]);
         pw[1] = fmax(pw[1], pt[1]);
@@ -392,7 +456,9 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         pw[3] = fmax(pw[3], pt[3]);
       }
       pw[0] = warp_sum(pw[0]);  // (lane partials of the warp's tiles, in tile order per lane)
+      GRP_STAMP(2);
       group_partials(pw, G, lane);
+      GRP_STAMP(3);
       err = pw[0];
       const bool ps_oor = pw[1] > 0.0;  // (epi_rows<.., EXT = false>: out-of-range flag)
       if (j == 0 && lane == 0) d.hist[(long long)prob * d.itr_max + it] = err;
@@ -405,20 +471,25 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
       }
       // ---- half B: phi <- u / K' psi (_kernels.py:315-349)
       G.sync();  // every psi of the problem is final
+      GRP_STAMP(4);
       proxy_fence();
-      group_carries(d.RB, a.S4, b, e, G, lane);
+      group_carries(d.RB, a.S4, b, e, G, lane, stash_ok ? stash : nullptr);
+      GRP_STAMP(5);
       double qw[4] = {0.0, 0.0, INFINITY, -1.0};
       TileStep ts1 = d.steps[b < e ? b : 0];
       for (int t = b; t < e; ++t) {
         double pt[4];
         const TileStep nts = d.steps[t + 1 < e ? t + 1 : t];
-        group_tile<1>(d, t, ts1, t + 1 < e, nts, wsm, mb, lane, phase, a.S4 + 4 * (size_t)t, pt);
+        group_tile<1>(d, t, ts1, t + 1 < e, nts, wsm, mb, lane, phase, a.S4 + 4 * (size_t)t, pt,
+                      t - b < STASH ? stash + 2 * (t - b) : nullptr);
         ts1 = nts;
         qw[1] = fmax(qw[1], pt[1]);
         qw[2] = fmin(qw[2], pt[2]);
         qw[3] = fmax(qw[3], pt[3]);
       }
+      GRP_STAMP(6);
       group_partials(qw, G, lane);
+      GRP_STAMP(7);
       const bool ph_oor = qw[1] > 0.0;
       const int k = ++it;  // solver.py:177
       if (qw[3] >= 0.0) {
@@ -437,6 +508,7 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         n_abs += 1;
         G.sync();  // every phi of the problem is final
         group_build(d, 0, b, e, wsm, tab, sbuf, absorbed);
+        stash_ok = false;  // (absorb_core's area overlaps the stash; the maps are in global)
         G.sync();  // every tile has read the old shifts and scalings
         sbuf ^= 1;
         absorbed = true;
