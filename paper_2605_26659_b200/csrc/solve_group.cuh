@@ -37,27 +37,28 @@ constexpr int WSTASH = WST + 2 * 5 * STASH;
 constexpr int WREG = WSTASH > WSM ? WSTASH : WSM;  // shared doubles per warp (step / absorb)
 
 #ifdef FB_DBG_GRP
-// (timing experiment: globaltimer stamps of one iteration's phases by warp 0
-// of problem 0, read by finom_grp_read; tools/grp_time.py)
+// (timing experiment: every group's warp 0 adds the globaltimer durations of
+// its iteration phases into g_grp[k] (k = 0..6), g_grp[15] counts the
+// iterations; finom_grp_read, tools/grp_time.py)
 __device__ unsigned long long g_grp[16];
-__device__ int g_grp_on;
-__device__ __forceinline__ void grp_stamp(int k) {
+__device__ __forceinline__ unsigned long long grp_now() {
   unsigned long long t_;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-  g_grp[k] = t_;
+  return t_;
 }
-#define GRP_STAMP(k)                                                    \
-  do {                                                                  \
-    if (prob == 0 && j == 0 && lane == 0 && it == 20) grp_stamp(k);     \
-  } while (0)
-#define GRP_STAMP_IN(k)                                                 \
-  do {                                                                  \
-    if (g_grp_on == (int)(blockIdx.x * 32 + (threadIdx.x >> 5)) + 1 && lane == 0) grp_stamp(k); \
+#define GRP_STAMP(k)                                       \
+  do {                                                     \
+    if (j == 0 && lane == 0) {                             \
+      const unsigned long long n_ = grp_now();             \
+      if (k > 0) atomicAdd(&g_grp[k - 1], n_ - grp_t);     \
+      else atomicAdd(&g_grp[15], 1ull);                    \
+      grp_t = n_;                                          \
+    }                                                      \
   } while (0)
 #else
 #define GRP_STAMP(k)
-#define GRP_STAMP_IN(k)
 #endif
+#define GRP_STAMP_IN(k)
 
 struct GX;
 struct GroupArgs {
@@ -424,23 +425,19 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
     group_build(d, 1, b, e, wsm, tab, 0, false);
     G.sync();
     int it = 0, status = 0, fail_it = 0, sbuf = 0, n_abs = 0, converged = 0;
+#ifdef FB_DBG_GRP
+    unsigned long long grp_t = 0;
+#endif
     bool absorbed = false;
     bool stash_ok = false;  // (group_build wrote half A's maps to global only)
     Tf *stash = reinterpret_cast<Tf *>(wsm + WST);
     double err = 0.0;
     for (;;) {
       // ---- half A: psi <- v / K'^T phi (_kernels.py:278-314)
-#ifdef FB_DBG_GRP
-      if (prob == 0 && j == 0 && lane == 0)
-        g_grp_on = it == 20 ? (int)(blockIdx.x * 32 + (threadIdx.x >> 5)) + 1 : 0;
-#endif
       GRP_STAMP(0);
       proxy_fence();
       group_carries(d.RA, a.S4, b, e, G, lane, stash_ok ? stash : nullptr);
       stash_ok = true;  // (half A's tiles write it for half B)
-#ifdef FB_DBG_GRP
-      if (prob == 0 && j == 0 && lane == 0) g_grp_on = 0;
-#endif
       GRP_STAMP(1);
       double pw[4] = {0.0, 0.0, INFINITY, -1.0};
       TileStep ts = d.steps[b < e ? b : 0];
@@ -470,7 +467,8 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         break;
       }
       // ---- half B: phi <- u / K' psi (_kernels.py:315-349)
-      G.sync();  // every psi of the problem is final
+      // (every psi of the problem is final: each warp passed the partials'
+      // barrier after its tiles)
       GRP_STAMP(4);
       proxy_fence();
       group_carries(d.RB, a.S4, b, e, G, lane, stash_ok ? stash : nullptr);
@@ -502,7 +500,9 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         converged = 1;
         break;
       }
+      bool reb = false;
       if (d.stabilize && (ph_oor || ps_oor)) {  // solver.py:193-198: absorb, phi = psi = 1
+        reb = true;
         if (j == 0 && lane == 0 && d.absorb_its)
           d.absorb_its[(long long)prob * d.itr_max + n_abs] = k;
         n_abs += 1;
@@ -520,7 +520,9 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
         __syncwarp();
       }
       if (k >= d.itr_max) break;
-      G.sync();  // every phi / half-A map of the problem is final
+      // every phi / half-A map of the problem is final: the partials' barrier
+      // covers the tiles; after a rebuild, the resets above need one more
+      if (reb) G.sync();
     }
     // ---- k_final's part: shifts out, info, control block
     const double *As = d.A[sbuf], *Bs = d.B[sbuf];

@@ -23,17 +23,16 @@ else:
 lib = bs.plan.lib
 lib.finom_grp_read.argtypes = [ctypes.c_void_p]
 for rep in range(2):
-    bs.solve(40)
+    bs.solve(200)
     torch.cuda.synchronize()
 out = np.zeros(16)
 lib.finom_grp_read(_lib.ptr(out))
-t = (out[:8] - out[0]) / 1e3
+its = out[15]
 names = ["A carries", "A tiles", "A partials", "sync", "B carries", "B tiles", "B partials"]
-print(which, "group", lib.finom_solve1d_group(bs.plan.handle), "tiles/warp",
-      bs.plan.info()["tiles"] // max(1, abs(lib.finom_solve1d_group(bs.plan.handle))))
+print(which, "group", lib.finom_solve1d_group(bs.plan.handle), "iterations timed", int(its))
+tot = 0.0
 for k, nm in enumerate(names):
-    print("  %-12s %8.2f us" % (nm, t[k + 1] - t[k]))
-print("  half A+B    %8.2f us" % (t[7] - t[0]))
-c = (out[8:12] - out[0]) / 1e3
-print("  inside half A carries (from its start): node loads %.2f, scan %.2f, barrier %.2f, "
-      "prefix %.2f us" % (c[0], c[1], c[2], c[3]))
+    v = out[k] / its / 1e3
+    tot += v
+    print("  %-12s %8.2f us (mean over groups and iterations)" % (nm, v))
+print("  sum         %8.2f us" % tot)
