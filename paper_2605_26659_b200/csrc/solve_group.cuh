@@ -254,7 +254,7 @@ __device__ __forceinline__ void proxy_fence() {
 // next tile's descriptor (prefetched into L2 during this tile), if any.
 template <int HALF>
 __device__ __forceinline__ void group_tile(const Dev &d, int t, const TileStep &ts, bool next,
-                                           const TileStep &nts, double *wsm,
+                                           int tn, const TileStep &nts, double *wsm,
                                            unsigned long long *bar, int lane, unsigned &phase,
                                            const double *init, double *part, Tf *stash) {
   TileIn in;
@@ -279,7 +279,7 @@ __device__ __forceinline__ void group_tile(const Dev &d, int t, const TileStep &
     vec_issue(in.cv, Cs, vc, bar);
     // (measured at config 5: prefetch distance 2 1074 ms, record only
     // 1050, distance 1 with the vectors 1047 ms per solve)
-    if (next) group_prefetch<HALF>(d, t + 1, nts);
+    if (next) group_prefetch<HALF>(d, tn, nts);
   }
   // lanes 0 / 4: the incoming states (forward / backward), off the walk's path
   double st0 = 0.0, st1 = 0.0;
@@ -444,8 +444,8 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
       for (int t = b; t < e; ++t) {
         double pt[4];
         const TileStep nts = d.steps[t + 1 < e ? t + 1 : t];
-        group_tile<0>(d, t, ts, t + 1 < e, nts, wsm, mb, lane, phase, a.S4 + 4 * (size_t)t, pt,
-                      t - b < STASH ? stash + 2 * (t - b) : nullptr);
+        group_tile<0>(d, t, ts, t + 1 < e, t + 1, nts, wsm, mb, lane, phase,
+                      a.S4 + 4 * (size_t)t, pt, t - b < STASH ? stash + 2 * (t - b) : nullptr);
         ts = nts;
         pw[0] = __dadd_rn(pw[0], pt[0]);
         pw[1] = fmax(pw[1], pt[1]);
@@ -474,12 +474,15 @@ __global__ void __launch_bounds__(GTHR, 1) k_solve_group(GroupArgs a) {
       group_carries(d.RB, a.S4, b, e, G, lane, stash_ok ? stash : nullptr);
       GRP_STAMP(5);
       double qw[4] = {0.0, 0.0, INFINITY, -1.0};
-      TileStep ts1 = d.steps[b < e ? b : 0];
-      for (int t = b; t < e; ++t) {
+      // half B walks the warp's tiles backwards (half A forwards): its first
+      // tiles read the scalings half A wrote last, still in L2 (and half A's
+      // first ones half B's last); config 5: 1003.5 -> 995 ms
+      TileStep ts1 = d.steps[e > b ? e - 1 : 0];
+      for (int t = e - 1; t >= b; --t) {
         double pt[4];
-        const TileStep nts = d.steps[t + 1 < e ? t + 1 : t];
-        group_tile<1>(d, t, ts1, t + 1 < e, nts, wsm, mb, lane, phase, a.S4 + 4 * (size_t)t, pt,
-                      t - b < STASH ? stash + 2 * (t - b) : nullptr);
+        const TileStep nts = d.steps[t - 1 >= b ? t - 1 : t];
+        group_tile<1>(d, t, ts1, t - 1 >= b, t - 1, nts, wsm, mb, lane, phase,
+                      a.S4 + 4 * (size_t)t, pt, t - b < STASH ? stash + 2 * (t - b) : nullptr);
         ts1 = nts;
         qw[1] = fmax(qw[1], pt[1]);
         qw[2] = fmin(qw[2], pt[2]);
