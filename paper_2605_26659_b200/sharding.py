@@ -8,6 +8,8 @@ replicas.  The solve function is injectable so the partition / gather
 logic is testable on CPU with the gloo backend (tests/test_sharding_cpu.py).
 """
 
+import os
+
 import numpy as np
 
 
@@ -302,12 +304,19 @@ def _check_grids(source, target):
         raise ConfigError("row sharding needs source and target grids with the same x nodes")
 
 
-def _device_loop(config, dev, iterate, absorb):
+LAST_LOOP = {}  # (the last _device_loop: iterations replayed from captured graphs, for tests)
+
+
+def _device_loop(config, dev, iterate, absorb, capture=False):
     """run_driver over a sharded 2D iteration with the decisions on the device:
     iterate(dyn, ctl, hist, abs_its) queues both halves, the partials'
     exchange and finom_grid2d_decide; the host reads the 8-word control block
-    once per iteration (absorb when flagged, stop when done).  Returns (it,
-    converged, status, hist, absorb_its)."""
+    once per iteration (absorb when flagged, stop when done).  capture: after
+    one eager iteration (NCCL communicators up, buffers allocated) the
+    iteration -- its kernels and its NCCL all-gathers -- is captured once per
+    kernel form (before / after the first absorption) into a CUDA graph and
+    replayed (FINOM_GRAPH_SHARD=0: eager).  Returns (it, converged, status,
+    hist, absorb_its)."""
     import torch
     itr = int(config.itr_max)
     ctl = torch.zeros(8, dtype=torch.int64, device=dev)
@@ -315,8 +324,25 @@ def _device_loop(config, dev, iterate, absorb):
     abs_its = torch.zeros(itr, dtype=torch.int64, device=dev)
     ctl_h = torch.zeros(8, dtype=torch.int64).pin_memory()
     dyn = False
+    capture = capture and os.environ.get("FINOM_GRAPH_SHARD", "1") != "0"
+    graphs = {}
+    first = True
     while True:
-        iterate(dyn, ctl, hist, abs_its)
+        g = graphs.get(dyn) if capture and not first else None
+        if capture and not first and g is None:
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    iterate(dyn, ctl, hist, abs_its)
+                graphs[dyn] = g
+            except Exception:  # noqa: BLE001  (capture unsupported: stay eager)
+                capture, g = False, None
+                torch.cuda.synchronize()
+        if g is not None:
+            g.replay()
+        else:
+            iterate(dyn, ctl, hist, abs_its)
+        first = False
         ctl_h.copy_(ctl, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         c = ctl_h.numpy()
@@ -326,6 +352,8 @@ def _device_loop(config, dev, iterate, absorb):
         if c[4]:
             break
     it, status, conv, nab = int(c[0]), int(c[1]), bool(c[2]), int(c[5])
+    LAST_LOOP.clear()
+    LAST_LOOP.update(graphs=len(graphs), captured=capture)
     return it, conv, status, hist[:it].cpu().numpy().tolist(), abs_its[:nab].cpu().tolist()
 
 
@@ -374,7 +402,7 @@ def sinkhorn_2d_row_sharded(source, target, u, v, config, group=None):
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    it, conv, status, hist, abs_its = _device_loop(config, dev, iterate, absorb)
+    it, conv, status, hist, abs_its = _device_loop(config, dev, iterate, absorb, capture=True)
     torch.cuda.synchronize()
     wall = max_over_ranks(time.perf_counter() - t0)
     out = {}

@@ -175,6 +175,9 @@ def test_row_sharded_2d_nccl_world1():
                                 world_size=1, device_id=torch.device("cuda", 0))
     try:
         a = S.sinkhorn_2d_row_sharded(src, tgt, fb.Measure2D(U), fb.Measure2D(V), cfg)
+        # the iteration (kernels + NCCL all-gathers) replayed from CUDA graphs,
+        # one per kernel form (before / after the first absorption)
+        assert S.LAST_LOOP["captured"] and S.LAST_LOOP["graphs"] == 2, S.LAST_LOOP
     finally:
         if own:
             dist.destroy_process_group()
