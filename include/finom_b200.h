@@ -284,6 +284,14 @@ int finom_seg1d_finish(finom_seg1d *seg, int half, const double *in_dev, const d
 int finom_seg1d_absorb(finom_seg1d *seg, int side, double *shift_dev, const double *W_dev,
                        const double *SC_dev, const int32_t *prv_dev, const int32_t *nxt_dev,
                        void *stream);
+/* run_driver's decisions (solver.py:173-198) of a distributed-scan iteration
+ * on the device, as finom_grid2d_decide (ctl, hist, absorb_its the same),
+ * with the segments' partials (err, max, min, status or -1) combined in rank
+ * order and the LAST failing segment's status reported (the reference's
+ * loops run downward). */
+int finom_seg1d_decide(const double *parts_a, const double *parts_b, int R, int64_t *ctl,
+                       double *hist, int64_t *absorb_its, int64_t itr_max, double tol,
+                       int stabilize, double absorb_threshold, void *stream);
 
 /* ---- Row-sharded 2D grids (no reference equivalent) ----
  * One handle per rank for source == target grids x[n] x (y1[m1] | y2[m2]),

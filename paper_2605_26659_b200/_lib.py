@@ -93,6 +93,8 @@ SIGNATURES = {
     "finom_grid2d_absorb_nb": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "finom_grid2d_decide": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int,
                                      _c_dbl, _vp]),
+    "finom_seg1d_decide": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int,
+                                    _c_dbl, _vp]),
     "finom_grid2d_absorb": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                      _vp]),
 }

@@ -552,6 +552,14 @@ class Segment1D:
                 "finom_seg1d_finish")
         return self.part
 
+    def decide(self, parts_a, parts_b, R, ctl, hist, abs_its, config):
+        """run_driver's decisions of the iteration on the device (finom_seg1d_decide)."""
+        L, P = self._lib, self._lib.ptr
+        L.check(self.lib.finom_seg1d_decide(
+            P(parts_a), P(parts_b), R, P(ctl), P(hist), P(abs_its), int(config.itr_max),
+            float(config.tol), int(bool(config.stabilize)), float(config.absorb_threshold),
+            L.stream_ptr()), "finom_seg1d_decide")
+
     def absorb(self, side, sc_whole):
         L, P = self._lib, self._lib.ptr
         sh, W = (self.A, self.U) if side == 0 else (self.B, self.V)
@@ -607,12 +615,14 @@ def sinkhorn_1d_segmented(x, y, u, v, config, group=None):
     sg = Segment1D(X, Y, Uw, Vw, config.epsilon, R, r)
     dev = sg.PHI.device
     tot_all = torch.empty(10 * R, dtype=torch.float64, device=dev)
-    parts = torch.empty(4 * R, dtype=torch.float64, device=dev)
+    parts = {h: torch.empty(4 * R, dtype=torch.float64, device=dev) for h in (0, 1)}
 
-    def phase(half, dyn):
-        dist.all_gather_into_tensor(tot_all, sg.pre(half).contiguous(), group=group)
-        dist.all_gather_into_tensor(parts, sg.finish(half, tot_all).contiguous(), group=group)
-        return combine_parts_1d(parts.cpu().numpy())
+    def iterate(dyn, ctl, hist, abs_its):  # (device-resident: decisions in finom_seg1d_decide)
+        for half in (0, 1):
+            dist.all_gather_into_tensor(tot_all, sg.pre(half).contiguous(), group=group)
+            dist.all_gather_into_tensor(parts[half], sg.finish(half, tot_all).contiguous(),
+                                        group=group)
+        sg.decide(parts[0], parts[1], R, ctl, hist, abs_its, config)
 
     wins = [None] * R
     dist.all_gather_object(wins, sg.window, group=group)
@@ -632,7 +642,7 @@ def sinkhorn_1d_segmented(x, y, u, v, config, group=None):
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    it, conv, status, hist, abs_its = run_driver_2d(phase, absorb, config)
+    it, conv, status, hist, abs_its = _device_loop(config, dev, iterate, absorb, capture=True)
     torch.cuda.synchronize()
     wall = max_over_ranks(time.perf_counter() - t0)
     phi, psi = gather_whole(sg.PHI, 0), gather_whole(sg.PSI, 1)
@@ -654,10 +664,12 @@ def sinkhorn_1d_segmented_sim(x, y, u, v, config, R):
     segs = [Segment1D(X, Y, Uw, Vw, config.epsilon, R, k) for k in range(R)]
     wins = [s.window for s in segs]
 
-    def phase(half, dyn):
-        tot_all = torch.cat([s.pre(half).clone() for s in segs])
-        parts = [s.finish(half, tot_all).cpu().numpy() for s in segs]
-        return combine_parts_1d(parts)
+    def iterate(dyn, ctl, hist, abs_its):
+        parts = []
+        for half in (0, 1):
+            tot_all = torch.cat([s.pre(half).clone() for s in segs])
+            parts.append(torch.cat([s.finish(half, tot_all).clone() for s in segs]))
+        segs[0].decide(parts[0], parts[1], R, ctl, hist, abs_its, config)
 
     def absorb():
         for side in (0, 1):
@@ -670,7 +682,7 @@ def sinkhorn_1d_segmented_sim(x, y, u, v, config, R):
             s.PSI.fill_(1.0)
             s.shifted = True
 
-    it, conv, status, hist, abs_its = run_driver_2d(phase, absorb, config)
+    it, conv, status, hist, abs_its = _device_loop(config, segs[0].PHI.device, iterate, absorb)
     torch.cuda.synchronize()
     phi = _assemble_1d([s.PHI.cpu().numpy() for s in segs], wins, 0)
     psi = _assemble_1d([s.PSI.cpu().numpy() for s in segs], wins, 1)

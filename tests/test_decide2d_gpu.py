@@ -8,7 +8,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _device_run(script, R, cfg):
+def _device_run(script, R, cfg, fn="finom_grid2d_decide"):
     import torch
     from paper_2605_26659_b200 import _lib
     lib = _lib.load()
@@ -20,7 +20,7 @@ def _device_run(script, R, cfg):
     while True:
         pa = torch.tensor(script[(it, 0)], dtype=torch.float64, device=dev)
         pb = torch.tensor(script[(it, 1)], dtype=torch.float64, device=dev)
-        _lib.check(lib.finom_grid2d_decide(_lib.ptr(pa), _lib.ptr(pb), R, _lib.ptr(ctl),
+        _lib.check(getattr(lib, fn)(_lib.ptr(pa), _lib.ptr(pb), R, _lib.ptr(ctl),
                                            _lib.ptr(hist), _lib.ptr(abs_its), cfg.itr_max,
                                            cfg.tol, int(cfg.stabilize), cfg.absorb_threshold,
                                            _lib.stream_ptr()), "decide")
@@ -33,12 +33,12 @@ def _device_run(script, R, cfg):
             abs_its[:int(c[5])].cpu().tolist())
 
 
-def _host_run(script, cfg):
+def _host_run(script, cfg, combine="combine_parts"):
     from paper_2605_26659_b200 import sharding as S
     state = {"it": 1}
 
     def phase(half, dyn):
-        out = S.combine_parts(np.asarray(script[(state["it"], half)]).reshape(-1, 4))
+        out = getattr(S, combine)(np.asarray(script[(state["it"], half)]).reshape(-1, 4))
         if half == 1:
             state["it"] += 1
         return out
@@ -79,3 +79,27 @@ def test_device_decisions_match_run_driver(case):
     assert dev[:3] == host[:3]
     assert dev[3] == host[3]  # (rank-order sums: bitwise)
     assert dev[4] == host[4]
+
+
+def test_seg1d_device_decisions_last_failing_segment():
+    """finom_seg1d_decide: partials carry a status, the LAST failing segment's
+    is reported (combine_parts_1d)."""
+    from paper_2605_26659_b200 import SolverConfig
+    R = 4
+    script = {}
+    for it in range(1, 9):
+        for half in (0, 1):
+            p = np.zeros((R, 4))
+            p[:, 0] = 0.01 * (R - np.arange(R)) / it
+            p[:, 1] = 1.5
+            p[:, 2] = 0.75
+            p[:, 3] = -1.0
+            script[(it, half)] = p.ravel().tolist()
+    script[(2, 1)][2 * 4 + 1] = 1e90       # absorption at iteration 2
+    script[(6, 0)][1 * 4 + 3] = 2.0        # NONFINITE on segment 1 ...
+    script[(6, 0)][3 * 4 + 3] = 1.0        # ... and ZERO_DENOM on segment 3: the last one wins
+    cfg = SolverConfig(epsilon=1e-2, itr_max=8, tol=0.0, stabilize=True, absorb_threshold=200.0)
+    dev = _device_run(script, R, cfg, fn="finom_seg1d_decide")
+    host = _host_run(script, cfg, combine="combine_parts_1d")
+    assert dev[:3] == host[:3] == (6, False, 1)
+    assert dev[3] == host[3] and dev[4] == host[4] == [2]

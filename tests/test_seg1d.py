@@ -140,6 +140,10 @@ def test_seg1d_nccl_world1():
                                 world_size=1, device_id=torch.device("cuda", 0))
     try:
         a = S.sinkhorn_1d_segmented(x, y, u, v, cfg)
+        # the iteration (kernels, NCCL all-gathers, device decisions) replayed
+        # from CUDA graphs, one per kernel form met after the first iteration
+        # (this case absorbs at iteration 1: the shifted form only)
+        assert S.LAST_LOOP["captured"] and S.LAST_LOOP["graphs"] >= 1, S.LAST_LOOP
     finally:
         if own:
             dist.destroy_process_group()
