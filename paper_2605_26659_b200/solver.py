@@ -369,9 +369,36 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
     comp = torch.cuda.current_stream()
     t0 = perf_counter()
     setup = [0.0]
+    ranges = _pipeline_ranges(nx)
+    # First-touch page faults of the fresh result arrays cost about as much as
+    # the device -> host copies into them: host threads touch each stage's
+    # slices while the device loops run (ctypes.memset releases the GIL), and
+    # a stage's results are fetched once its slices are touched.
+    import ctypes
+    import threading
+
+    def touch(lo, hi):
+        x0, x1, y0, y1 = xoff[lo], xoff[hi], yoff[lo], yoff[hi]
+        for arr, s0, s1 in ((phi, x0, x1), (psi, y0, y1), (a, x0, x1), (b, y0, y1),
+                            (hist, lo, hi), (abs_its, lo, hi)):
+            v = arr[s0:s1]
+            if v.nbytes:
+                ctypes.memset(v.ctypes.data, 0, v.nbytes)
+
+    touched = {k: threading.Event() for k in range(len(ranges))}
+    if len(ranges) > 1 and os.environ.get("FINOM_PIPE_TOUCH", "1") != "0":
+        def toucher():
+            for k, (lo, hi) in enumerate(ranges):
+                touch(lo, hi)
+                touched[k].set()
+        tt = threading.Thread(target=toucher, daemon=True)
+    else:
+        tt = None
 
     def fetch(stage):
-        lo, hi, bs, done = stage
+        lo, hi, bs, done, k = stage
+        if tt is not None:
+            touched[k].wait()
         done.synchronize()
         x0, x1, y0, y1 = xoff[lo], xoff[hi], yoff[lo], yoff[hi]
         for h, d in ((phi[x0:x1], bs.phi), (psi[y0:y1], bs.psi), (a[x0:x1], bs.a),
@@ -383,7 +410,7 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
     pending = None
     marks = []
     stages = []  # (kept to the end: destroying a plan waits for every stream it ran on)
-    for lo, hi in _pipeline_ranges(nx):
+    for si, (lo, hi) in enumerate(ranges):
         ts = perf_counter()
         # plan (host tiling + H2D) and weights on a stream of the stage's own:
         # nothing queued on it can make its pageable copies wait for the
@@ -405,6 +432,8 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
         bs.compute_cost()
         done = torch.cuda.Event(enable_timing=True)
         done.record(comp)
+        if si == 0 and tt is not None:
+            tt.start()  # (after the first stage's loop is queued: the host is idle meanwhile)
         if verbose:
             marks.append((start, done))
         tq = perf_counter()
@@ -413,7 +442,7 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
         if verbose:
             print("  stage %d-%d: prep %.1f ms, queue %.1f ms, fetch (previous) %.1f ms" % (
                 lo, hi, 1e3 * (tp - ts), 1e3 * (tq - tp), 1e3 * (perf_counter() - tq)), flush=True)
-        pending = (lo, hi, bs, done)
+        pending = (lo, hi, bs, done, si)
         stages.append(bs)
     fetch(pending)
     wall = perf_counter() - t0
@@ -424,7 +453,7 @@ def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):
     if verbose:
         print("sinkhorn_1d_batched: %d stage(s), setup %.1f ms, call %.1f ms; device loop "
               "+ cost per stage %s ms, gaps %s ms" % (
-                  len(_pipeline_ranges(nx)), 1e3 * setup[0], 1e3 * wall,
+                  len(ranges), 1e3 * setup[0], 1e3 * wall,
                   ["%.1f" % a.elapsed_time(b) for a, b in marks],
                   ["%.1f" % marks[k][1].elapsed_time(marks[k + 1][0])
                    for k in range(len(marks) - 1)]), flush=True)
