@@ -21,11 +21,12 @@ cfg = fb.SolverConfig(epsilon=1.0, itr_max=200, tol=0.0, stabilize=True)
 for st in sys.argv[1:] or ["1", "8"]:
     os.environ["FINOM_PIPE_STAGES"] = st
     ts = []
-    for r in range(3):
+    for r in range(int(os.environ.get("FINOM_REPS", "3"))):
         torch.cuda.synchronize()
         t = time.perf_counter()
         sols = fb.sinkhorn_1d_batched(xs, ys, us, vs, cfg, epsilons=eps)
         ts.append(time.perf_counter() - t)
         del sols
-    print("stages %s: %s s  e2e %.3e pts*it/s" % (st, ["%.3f" % x for x in ts],
-                                                  B * 16384 * 200 / min(ts)), flush=True)
+    print("stages %s: %s s  e2e %.3e pts*it/s (best), median %.3f s" % (
+        st, ["%.3f" % x for x in ts], B * 16384 * 200 / min(ts), sorted(ts)[len(ts) // 2]),
+        flush=True)
