@@ -462,4 +462,197 @@ __global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
   griddep_launch();
 }
 
+// Short lines (tl <= SQ_FUSE = 4 tiles, config 3): one CTA per LPC lines runs a
+// whole sweep -- k_sq_pre's tile maps, k_sq_scan's single-chunk warp scan and
+// k_sq_apply, with the same operations in the same order (bitwise equal to
+// the three-kernel path), the maps exchanged through shared memory.  Warp w
+// takes tile w / LPC of line p0 + w % LPC; the input tile is read once (the
+// pre phase's registers feed the apply phase) and the records of both phases
+// are issued before the first dependent read.  The transposed output and the
+// fused scaling update run per tile over the tile's LPC warps (named barrier
+// 1 + tile), so the partials are k_sq_apply's, per (line group, tile).
+constexpr int SQ_FUSE = 4;
+template <int LPC>
+__global__ void __launch_bounds__(32 * LPC * SQ_FUSE) k_sq_fused(SqArgs a) {
+  extern __shared__ __align__(16) double fsm[];
+  constexpr int GT = 32 * LPC;  // threads per tile group
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = warp / LPC, l = warp % LPC, tl = a.tl;
+  const int p0 = blockIdx.x * LPC, p = p0 + l;
+  double *so = fsm + (size_t)warp * SQX;
+  Tf *maps = reinterpret_cast<Tf *>(fsm + (size_t)LPC * tl * SQX);  // [LPC][tl][2]
+  const bool live = p < a.lines;
+  const size_t tile = (size_t)p * tl + t;
+  const size_t rec = a.shared || a.D ? (size_t)t : tile;
+  double2 f0[SQE], f1[SQE];
+  double x[SQE + 1];
+  griddep_wait();
+  if (live) {
+    const double2 *W = a.W + rec * SQW;
+    sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, so, x);
+    // ---- k_sq_pre: the tile's maps
+    double cf = 0.0, cb = 0.0;
+    if (a.D) {  // split records: shared ratios and raw W, the line's (delta, mu)
+      const double2 *D = a.D + tile * SQW;
+#pragma unroll
+      for (int k = 0; k < SQE; ++k) {
+        const double2 dk = __ldcs(D + k * 32 + lane);
+        const double2 w = __ldg(W + k * 32 + lane);
+        f0[k].y = dk.x;
+        f1[k].y = dk.y;
+        cf = __fma_rn(__dmul_rn(dk.x, w.x), x[k], cf);
+        cb = __fma_rn(__dmul_rn(dk.y, w.y), x[k + 1], cb);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < SQE; ++k) {
+        const double2 w = __ldg(W + k * 32 + lane);
+        cf = __fma_rn(w.x, x[k], cf);
+        cb = __fma_rn(w.y, x[k + 1], cb);
+      }
+    }
+    cf = warp_sum(cf);
+    cb = warp_sum(cb);
+    if (lane == 0) {
+      const double2 s = __ldg(a.S + rec);
+      maps[2 * (l * tl + t)] = Tf{s.x, 0.0, cf, 1.0, 0.0};
+      maps[2 * (l * tl + t) + 1] = Tf{s.y, 0.0, cb, 1.0, 0.0};
+    }
+  }
+  __syncthreads();
+  if (live) {
+    // ---- k_sq_scan (one chunk), then lane t's exclusive maps applied to zero
+    const bool have = lane < tl;
+    const Tf f = have ? maps[2 * (l * tl + lane)] : tf_id();
+    const Tf b = have ? maps[2 * (l * tl + lane) + 1] : tf_id();
+    Tf xf, xb, totf, totb;
+    warp_scan2<true>(f, b, xf, xb, totf, totb);
+    const Tf X = tf_cat_g(tf_id(), xf);
+    const double pv = (gm(X.A, 0.0) + 0.0) + X.C, qv = (gm(xb.A, 0.0) + 0.0) + xb.C;
+    double pin = __shfl_sync(0xffffffffu, pv, t), qin = __shfl_sync(0xffffffffu, qv, t);
+    // ---- k_sq_apply (its records)
+    const double2 *F = a.F + rec * SQF;
+    if (a.D) {
+#pragma unroll
+      for (int k = 0; k < SQE; ++k) {
+        f0[k].x = __ldg(&F[k * 32 + lane].x);
+        f1[k].x = __ldg(&F[(SQE + k) * 32 + lane].x);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < SQE; ++k) {
+        f0[k] = __ldcs(F + k * 32 + lane);
+        f1[k] = __ldcs(F + (SQE + k) * 32 + lane);
+      }
+    }
+    double af = 1.0, cf = 0.0, ab = 1.0, cb = 0.0;
+#pragma unroll
+    for (int k = 0; k < SQE; ++k) {
+      f0[k].y = __dmul_rn(f0[k].y, x[k]);
+      f1[k].y = __dmul_rn(f1[k].y, x[k + 1]);
+      af = __dmul_rn(f0[k].x, af);
+      cf = __dadd_rn(__dmul_rn(f0[k].x, cf), f0[k].y);
+    }
+#pragma unroll
+    for (int k = SQE - 1; k >= 0; --k) {
+      ab = __dmul_rn(f1[k].x, ab);
+      cb = __dadd_rn(__dmul_rn(f1[k].x, cb), f1[k].y);
+    }
+    if (lane == 0) { cf = __fma_rn(af, pin, cf); af = 0.0; }
+    if (lane == 31) { cb = __fma_rn(ab, qin, cb); ab = 0.0; }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double oa = __shfl_up_sync(0xffffffffu, af, off);
+      const double oc = __shfl_up_sync(0xffffffffu, cf, off);
+      const double ob = __shfl_down_sync(0xffffffffu, ab, off);
+      const double od = __shfl_down_sync(0xffffffffu, cb, off);
+      if (lane >= off) { cf = __fma_rn(af, oc, cf); af = __dmul_rn(af, oa); }
+      if (lane + off < 32) { cb = __fma_rn(ab, od, cb); ab = __dmul_rn(ab, ob); }
+    }
+    double pp = __shfl_up_sync(0xffffffffu, cf, 1), qq = __shfl_down_sync(0xffffffffu, cb, 1);
+    if (lane == 0) pp = pin;
+    if (lane == 31) qq = qin;
+#pragma unroll
+    for (int k = 0; k < SQE; ++k) {
+      pp = __dadd_rn(__dmul_rn(f0[k].x, pp), f0[k].y);
+      f0[k].y = pp;
+    }
+#pragma unroll
+    for (int k = SQE - 1; k >= 0; --k) {
+      qq = __dadd_rn(__dmul_rn(f1[k].x, qq), f1[k].y);
+      so[SQE * lane + k] = __dadd_rn(f0[k].y, qq);
+    }
+  }
+  // ---- per tile: transposed write or the fused scaling update (k_sq_apply's)
+  const int tid = threadIdx.x - GT * t;  // thread within the tile's group
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + t), "r"(GT) : "memory");
+  const int cnt = min(SQT, a.n - t * SQT);
+  double *sg = fsm + (size_t)t * LPC * SQX;  // the group's LPC output rows
+  if (!a.ew) {
+    for (int k = tid; k < cnt * LPC; k += GT) {
+      const int i = k / LPC, w = k % LPC;
+      if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = sg[w * SQX + i];
+    }
+    griddep_launch();
+    return;
+  }
+  double err = 0.0, vmax = 0.0, vmin = INFINITY;
+  long long fail = LLONG_MAX;
+  constexpr int EPER = SQT * LPC / GT;
+  double wq[EPER], sq[EPER];
+#pragma unroll
+  for (int q = 0; q < EPER; ++q) {
+    const int k = tid + q * GT, i = k / LPC, w = k % LPC;
+    const bool lv = k < cnt * LPC && p0 + w < a.lines;
+    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+    wq[q] = lv ? __ldcs(a.ew + idx) : 0.0;
+    sq[q] = lv && a.eerr ? __ldcs(a.esc + idx) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < EPER; ++q) {
+    const int k = tid + q * GT, i = k / LPC, w = k % LPC;
+    if (k >= cnt * LPC || p0 + w >= a.lines) continue;
+    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+    const long long kg = a.ek0 + p0 + w + (long long)a.eng * (t * SQT + i);
+    const double wv = wq[q], tt = sg[w * SQX + i];
+    if (a.eerr) err = __dadd_rn(err, fabs(__dsub_rn(__dmul_rn(sq[q], tt), wv)));
+    double nv;
+    if (tt == 0.0) {
+      if (wv > 0.0) fail = min(fail, (kg << 2) | ST_ZD);
+      nv = 0.0;
+    } else {
+      nv = __ddiv_rn(wv, tt);
+      if (!isfinite(nv)) fail = min(fail, (kg << 2) | ST_NF);
+      else if (wv > 0.0) {
+        vmax = fmax(vmax, nv);
+        vmin = fmin(vmin, nv);
+      }
+    }
+    a.esc[idx] = nv;
+  }
+  // epi_block_part over the group's LPC warps (same fold order as a LPC-warp CTA)
+  __shared__ EpiPart sp[SQ_FUSE][LPC];
+  err = warp_sum(err);
+  vmax = warp_max(vmax);
+  vmin = warp_min(vmin);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const long long o = __shfl_xor_sync(0xffffffffu, fail, off);
+    fail = o < fail ? o : fail;
+  }
+  if (lane == 0) sp[t][l] = EpiPart{err, vmax, vmin, fail};
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + t), "r"(GT) : "memory");
+  if (tid == 0) {
+    EpiPart r{0.0, 0.0, INFINITY, LLONG_MAX};
+    for (int w = 0; w < LPC; ++w) {
+      r.err += sp[t][w].err;
+      r.vmax = fmax(r.vmax, sp[t][w].vmax);
+      r.vmin = fmin(r.vmin, sp[t][w].vmin);
+      r.fail = sp[t][w].fail < r.fail ? sp[t][w].fail : r.fail;
+    }
+    a.epart[(size_t)blockIdx.x * tl + t] = r;
+  }
+  griddep_launch();
+}
+
 }  // namespace fb

@@ -188,12 +188,16 @@ def test_row_sharded_2d_nccl_world1():
     assert abs(a.cost - b.cost) <= 1e-11 * abs(b.cost)
 
 
-@pytest.mark.parametrize("env", [{"FB_GRAPH2D": "0"}, {"FB_SQ_SPLIT": "0"}, {"FB_SQ": "0"}])
-def test_2d_loop_variants_agree(monkeypatch, env):
-    """The device-looped graph vs the host-stepped loop (bitwise: same kernels),
-    split vs full square-sweep records and square vs general sweeps (1e-12):
-    absorbed config-3-style grid with a zero-mass stretch and a tol stop."""
-    x1, y1, x2, y2, U, V, eps = W.config3(n=96)
+@pytest.mark.parametrize("env,n", [({"FB_GRAPH2D": "0"}, 96), ({"FB_SQ_SPLIT": "0"}, 96),
+                                   ({"FB_SQ": "0"}, 96), ({"FB_SQ_FUSE": "0"}, 96),
+                                   ({"FB_SQ_FUSE": "0"}, 700)])
+def test_2d_loop_variants_agree(monkeypatch, env, n):
+    """The device-looped graph vs the host-stepped loop and the fused short-line
+    sweep vs its three kernels (bitwise: the same operations), split vs full
+    square-sweep records and square vs general sweeps (1e-12): absorbed
+    config-3-style grid with a zero-mass stretch and a tol stop (n = 700:
+    three ragged tiles per line)."""
+    x1, y1, x2, y2, U, V, eps = W.config3(n=n)
     U = U.copy()
     U[10:30, 40:50] = 0.0
     U /= U.sum()
@@ -206,7 +210,7 @@ def test_2d_loop_variants_agree(monkeypatch, env):
     assert base.iterations_run == alt.iterations_run and base.converged == alt.converged
     assert list(base.absorb_iterations) == list(alt.absorb_iterations)
     assert len(base.absorb_iterations) >= 1
-    tol = 0.0 if "FB_GRAPH2D" in env else 1e-12
+    tol = 0.0 if "FB_GRAPH2D" in env or "FB_SQ_FUSE" in env else 1e-12
     assert rel_inf(alt.phi, base.phi) <= tol and rel_inf(alt.psi, base.psi) <= tol
     assert abs(alt.cost - base.cost) <= max(tol, 1e-15) * abs(base.cost)
 
