@@ -103,12 +103,6 @@ struct SqArgs {
   // [k0, k0 + n) of lines of the whole mesh (Z already offset by k0)
   int k0;
   const double *carry;    // nullable: per line incoming (p, acc, q, accb) from the other shards
-  int pfd;                // k_sq_line: L2 prefetch distance in clusters (0: none)
-  // k_sq_chain: per (line, tile) 8 doubles -- the tile's maps (fwd A, fwd C,
-  // bwd A, bwd C) and, in the 5th slot, the launch epoch they belong to
-  double *chain;
-  const unsigned *epoch;  // the current launch's epoch (bumped by k_sq_bump before the launch)
-  int chk;                // k_sq_chain: 0 one CTA per tile; K > 0: pre / apply CTAs, K line groups apart
   double *tot;            // nullable: per line segment totals (forward Tf, backward Tf)
 };
 
@@ -658,488 +652,6 @@ __global__ void __launch_bounds__(32 * LPC * SQ_FUSE) k_sq_fused(SqArgs a) {
     }
     a.epart[(size_t)blockIdx.x * tl + t] = r;
   }
-  griddep_launch();
-}
-
-// Long lines (SQ_FUSE < tl <= TPC * 16 tiles, config 4): a thread-block
-// cluster runs the whole sweep of LPC lines -- CTA c of the cluster holds
-// tiles [c TPC, (c + 1) TPC) of each of the LPC lines, a warp per (tile,
-// line), the tile's factors and inputs in registers.  One pass over HBM: the
-// lane maps of both recurrences and their warp scans give the tile's maps
-// (no W records, no second read of the input or of the line's factors), the
-// maps are exchanged through distributed shared memory (every warp stores its
-// tile's maps into each CTA of the cluster, then a cluster barrier; the
-// maps of a line are then local reads),
-// a guarded warp scan over the line's tiles gives the tile's incoming P / Q,
-// and the lanes finish with the reference's recurrences ((r * p) + acc,
-// p + q; _kernels.py:65-67 / :80-87).  Per tile the transposed write or the
-// fused scaling update is k_sq_apply's (the same partials layout).
-// HBM bytes per point: the line's factors (32 per-line, 16 split, 0 shared)
-// + 8 in + 8 out -- against + 16 (W) + 8 (second input read) + the node
-// round trip of the three-kernel path.
-template <int LPC, int TPC>
-__global__ void __launch_bounds__(32 * LPC * TPC) k_sq_line(SqArgs a) {
-  constexpr int GT = 32 * LPC;  // threads per tile group
-  __shared__ double sm_so[LPC * TPC][SQX];
-  __shared__ double4 sm_maps[LPC][32];  // (fwd A, fwd C, bwd A, bwd C) per (line, tile of the line)
-  __shared__ EpiPart sm_sp[TPC][LPC];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned crank, csize, cid;
-  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
-  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
-  asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
-  const int tloc = warp / LPC, l = warp % LPC, tl = a.tl;
-  const int t = (int)crank * TPC + tloc;
-  const int p0 = (int)cid * LPC, p = p0 + l;
-  double *so = sm_so[warp];
-  const bool live = p < a.lines && t < tl;
-  const size_t tile = (size_t)p * tl + t;
-  double2 f0[SQE], f1[SQE];
-  double exa = 1.0, exc = 0.0, exb = 1.0, exd = 0.0;  // the lanes before / after this one
-  double ma = 1.0, mc = 0.0, mb = 1.0, md = 0.0;      // the tile's maps
-  // (every CTA of the cluster runs before any writes into its shared memory: waited on below)
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  griddep_wait();
-  if (a.pfd && t < tl) {
-    // L2 prefetch: the records and input of the tile this CTA slot takes a
-    // wave later (cluster cid + pfd), and this tile's scaling-update operands
-    const int pn = p + a.pfd * LPC;
-    if (pn < a.lines && lane == 0) {
-      const size_t tn = (size_t)pn * tl + t;
-      if (a.D) l2_prefetch(a.D + tn * SQW, sizeof(double2) * SQW);
-      else if (!a.shared) l2_prefetch(a.F + tn * SQF, sizeof(double2) * SQF);
-      const int cn = min(SQT + 1, a.n - t * SQT);
-      l2_prefetch(a.vin + (size_t)pn * a.n + t * SQT, sizeof(double) * cn);
-    }
-    if (a.ew && p0 < a.lines) {
-      const int cnt = min(SQT, a.n - t * SQT);
-      for (int i = l * 32 + lane; i < cnt; i += GT) {
-        const long long idx = (long long)(t * SQT + i) * a.lines + p0;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.ew + idx));
-        if (a.eerr) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.esc + idx));
-      }
-    }
-  }
-  if (live) {
-    const size_t rec = a.shared || a.D ? (size_t)t : tile;
-    const double2 *F = a.F + rec * SQF;
-    // the input first (its staging is the first dependent use), then the factors
-    double xr[SQE + 1];
-    {
-      const double *v = a.vin + (size_t)p * a.n;
-      const int t0 = t * SQT;
-#pragma unroll
-      for (int kk = 0; kk < SQE; ++kk) {
-        const int i = lane + 32 * kk;
-        xr[kk] = t0 + i < a.n ? __ldg(v + t0 + i) : 0.0;
-      }
-      xr[SQE] = lane == 0 && t0 + SQT < a.n ? __ldg(v + t0 + SQT) : 0.0;
-    }
-    if (a.D) {  // split records: shared ratios, the line's (delta, mu)
-      const double2 *D = a.D + tile * SQW;
-#pragma unroll
-      for (int k = 0; k < SQE; ++k) {
-        const double2 dk = __ldcs(D + k * 32 + lane);
-        f0[k] = make_double2(__ldg(&F[k * 32 + lane].x), dk.x);
-        f1[k] = make_double2(__ldg(&F[(SQE + k) * 32 + lane].x), dk.y);
-      }
-    } else if (a.shared) {
-#pragma unroll
-      for (int k = 0; k < SQE; ++k) {
-        f0[k] = __ldg(F + k * 32 + lane);
-        f1[k] = __ldg(F + (SQE + k) * 32 + lane);
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < SQE; ++k) {
-        f0[k] = __ldcs(F + k * 32 + lane);
-        f1[k] = __ldcs(F + (SQE + k) * 32 + lane);
-      }
-    }
-    double x[SQE + 1];
-#pragma unroll
-    for (int kk = 0; kk < SQE; ++kk) so[sq_pad(lane + 32 * kk)] = xr[kk];
-    if (lane == 0) so[sq_pad(SQT)] = xr[SQE];
-    __syncwarp();
-#pragma unroll
-    for (int kk = 0; kk <= SQE; ++kk) x[kk] = so[sq_pad(SQE * lane + kk)];
-    __syncwarp();
-    // lane maps: forward P_end = af P_in + cf, backward Q_first = ab Q_after + cb
-    double af = 1.0, cf = 0.0, ab = 1.0, cb = 0.0;
-#pragma unroll
-    for (int k = 0; k < SQE; ++k) {
-      f0[k].y = __dmul_rn(f0[k].y, x[k]);      // delta v
-      f1[k].y = __dmul_rn(f1[k].y, x[k + 1]);  // mu v_{+1}
-      af = __dmul_rn(f0[k].x, af);
-      cf = __dadd_rn(__dmul_rn(f0[k].x, cf), f0[k].y);
-    }
-#pragma unroll
-    for (int k = SQE - 1; k >= 0; --k) {
-      ab = __dmul_rn(f1[k].x, ab);
-      cb = __dadd_rn(__dmul_rn(f1[k].x, cb), f1[k].y);
-    }
-    // inclusive scans of the lane maps (in-tile products stay in range: no guards)
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const double oa = __shfl_up_sync(0xffffffffu, af, off);
-      const double oc = __shfl_up_sync(0xffffffffu, cf, off);
-      const double ob = __shfl_down_sync(0xffffffffu, ab, off);
-      const double od = __shfl_down_sync(0xffffffffu, cb, off);
-      if (lane >= off) { cf = __fma_rn(af, oc, cf); af = __dmul_rn(af, oa); }
-      if (lane + off < 32) { cb = __fma_rn(ab, od, cb); ab = __dmul_rn(ab, ob); }
-    }
-    // the tile's maps: lane 31 holds the forward one, lane 0 the backward one
-    ma = __shfl_sync(0xffffffffu, af, 31);
-    mc = __shfl_sync(0xffffffffu, cf, 31);
-    mb = __shfl_sync(0xffffffffu, ab, 0);
-    md = __shfl_sync(0xffffffffu, cb, 0);
-    exa = __shfl_up_sync(0xffffffffu, af, 1);
-    exc = __shfl_up_sync(0xffffffffu, cf, 1);
-    exb = __shfl_down_sync(0xffffffffu, ab, 1);
-    exd = __shfl_down_sync(0xffffffffu, cb, 1);
-    if (lane == 0) { exa = 1.0; exc = 0.0; }
-    if (lane == 31) { exb = 1.0; exd = 0.0; }
-  }
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // (the start barrier)
-  if (live) {
-    // push the tile's maps into every CTA of the cluster (distributed shared
-    // memory stores: lanes 0.. the forward map, lanes 16.. the backward one)
-    const unsigned dst = (unsigned)(lane & 15);
-    if (dst < csize) {
-      unsigned la = (unsigned)__cvta_generic_to_shared(&sm_maps[l][t]) + (lane >= 16 ? 16u : 0u), ra;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(dst));
-      asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(lane >= 16 ? mb : ma),
-                   "d"(lane >= 16 ? md : mc) : "memory");
-    }
-  }
-  // every tile map of the cluster's lines is written
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
-               ::: "memory");
-  if (live) {
-    // lane j: tile j's maps of this line
-    double fa = 1.0, fc = 0.0, ba = 1.0, bc = 0.0;
-    if (lane < tl) {
-      const double4 m = sm_maps[l][lane];
-      fa = m.x; fc = m.y; ba = m.z; bc = m.w;
-    }
-    // guarded inclusive scans along the line (cross-tile products may overflow
-    // or underflow: a structurally zero state stays zero, as tf_cat_g)
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const double oa = __shfl_up_sync(0xffffffffu, fa, off);
-      const double oc = __shfl_up_sync(0xffffffffu, fc, off);
-      const double ob = __shfl_down_sync(0xffffffffu, ba, off);
-      const double od = __shfl_down_sync(0xffffffffu, bc, off);
-      if (lane >= off) { fc = __dadd_rn(gm(fa, oc), fc); fa = gm(fa, oa); }
-      if (lane + off < 32) { bc = __dadd_rn(gm(ba, od), bc); ba = gm(ba, ob); }
-    }
-    // the tile's incoming states: P after tile t - 1, Q before tile t + 1 (zero at the line's ends)
-    double pin = __shfl_sync(0xffffffffu, fc, t > 0 ? t - 1 : 0);
-    double qin = __shfl_sync(0xffffffffu, bc, t + 1 < 32 ? t + 1 : 31);
-    if (t == 0) pin = 0.0;
-    if (t + 1 >= tl) qin = 0.0;
-    // this lane's incoming states, then the final recurrences
-    double pp = __dadd_rn(gm(exa, pin), exc), qq = __dadd_rn(gm(exb, qin), exd);
-#pragma unroll
-    for (int k = 0; k < SQE; ++k) {
-      pp = __dadd_rn(__dmul_rn(f0[k].x, pp), f0[k].y);
-      f0[k].y = pp;
-    }
-#pragma unroll
-    for (int k = SQE - 1; k >= 0; --k) {
-      qq = __dadd_rn(__dmul_rn(f1[k].x, qq), f1[k].y);
-      so[SQE * lane + k] = __dadd_rn(f0[k].y, qq);
-    }
-  }
-  // ---- per tile: transposed write or the fused scaling update (k_sq_apply's)
-  const int tid = threadIdx.x - GT * tloc;  // thread within the tile's group
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + tloc), "r"(GT) : "memory");
-  const int cnt = t < tl ? min(SQT, a.n - t * SQT) : 0;
-  double *sg = sm_so[tloc * LPC];  // the group's LPC output rows
-  if (!a.ew) {
-    for (int k = tid; k < cnt * LPC; k += GT) {
-      const int i = k / LPC, w = k % LPC;
-      if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = sg[w * SQX + i];
-    }
-  } else if (t < tl) {
-    double err = 0.0, vmax = 0.0, vmin = INFINITY;
-    long long fail = LLONG_MAX;
-    constexpr int EPER = SQT * LPC / GT;
-    double wq[EPER], sq[EPER];
-#pragma unroll
-    for (int q = 0; q < EPER; ++q) {
-      const int k = tid + q * GT, i = k / LPC, w = k % LPC;
-      const bool lv = k < cnt * LPC && p0 + w < a.lines;
-      const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
-      wq[q] = lv ? __ldcs(a.ew + idx) : 0.0;
-      sq[q] = lv && a.eerr ? __ldcs(a.esc + idx) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < EPER; ++q) {
-      const int k = tid + q * GT, i = k / LPC, w = k % LPC;
-      if (k >= cnt * LPC || p0 + w >= a.lines) continue;
-      const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
-      const long long kg = a.ek0 + p0 + w + (long long)a.eng * (t * SQT + i);
-      const double wv = wq[q], tt = sg[w * SQX + i];
-      if (a.eerr) err = __dadd_rn(err, fabs(__dsub_rn(__dmul_rn(sq[q], tt), wv)));
-      double nv;
-      if (tt == 0.0) {
-        if (wv > 0.0) fail = min(fail, (kg << 2) | ST_ZD);
-        nv = 0.0;
-      } else {
-        nv = __ddiv_rn(wv, tt);
-        if (!isfinite(nv)) fail = min(fail, (kg << 2) | ST_NF);
-        else if (wv > 0.0) {
-          vmax = fmax(vmax, nv);
-          vmin = fmin(vmin, nv);
-        }
-      }
-      a.esc[idx] = nv;
-    }
-    // epi_block_part over the group's LPC warps
-    err = warp_sum(err);
-    vmax = warp_max(vmax);
-    vmin = warp_min(vmin);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const long long o = __shfl_xor_sync(0xffffffffu, fail, off);
-      fail = o < fail ? o : fail;
-    }
-    if (lane == 0) sm_sp[tloc][l] = EpiPart{err, vmax, vmin, fail};
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + tloc), "r"(GT) : "memory");
-    if (tid == 0) {
-      EpiPart r{0.0, 0.0, INFINITY, LLONG_MAX};
-      for (int w = 0; w < LPC; ++w) {
-        r.err += sm_sp[tloc][w].err;
-        r.vmax = fmax(r.vmax, sm_sp[tloc][w].vmax);
-        r.vmin = fmin(r.vmin, sm_sp[tloc][w].vmin);
-        r.fail = sm_sp[tloc][w].fail < r.fail ? sm_sp[tloc][w].fail : r.fail;
-      }
-      a.epart[(size_t)cid * tl + t] = r;
-    }
-  }
-  griddep_launch();
-}
-
-// One pass per sweep without clusters: k_sq_apply's CTA (tile t of LPC lines,
-// a warp per line) computes its tile's maps from the factors it holds in
-// registers (as k_sq_line), publishes them (4 doubles + the launch epoch,
-// release store) and reads the other tiles' maps of its line (lane j polls
-// tile j's epoch with acquire loads), then the guarded warp scan over the
-// line's tiles, the final recurrences and the transposed write / fused
-// scaling update.  No k_sq_pre / k_sq_scan, no W records, no second read of
-// the input.  Forward progress: a CTA waits only for the tl CTAs of its own
-// line group, consecutive block indices (t fastest); blocks are dispatched in
-// index order (the assumption of single-pass look-back scans), so the group
-// is resident or about to be once any of its CTAs runs (tl <= 32, far below
-// the resident CTAs of the device).  Deterministic: the scan composes the
-// line's maps in tile order whatever the arrival order.
-__global__ void k_sq_bump(unsigned *epoch) { *epoch += 1; }
-
-template <int LPC>
-__global__ void __launch_bounds__(32 * LPC) k_sq_chain(SqArgs a) {
-  constexpr int THR = 32 * LPC;
-  __shared__ double so[LPC][SQX];  // input staging, then the tile's outputs
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tl = a.tl;
-  // roles (a.chk = K > 0): the grid is a sequence of slots u of 2 tl CTAs --
-  // tl "pre" CTAs of line group u (tile maps only: they pull the group's
-  // factors and input from HBM into L2 and publish) and tl "apply" CTAs of
-  // line group u - K (they find the maps published and re-read the group's
-  // data from L2), so no CTA waits while holding a tile in registers
-  int t = blockIdx.x % tl, grp = blockIdx.x / tl, role = 2;
-  if (a.chk) {
-    const int u = blockIdx.x / (2 * tl), r = blockIdx.x % (2 * tl);
-    role = r / tl;
-    t = r % tl;
-    grp = role == 0 ? u : u - a.chk;
-    if (grp < 0 || grp * LPC >= a.lines) return;
-  }
-  const int p0 = grp * LPC, p = p0 + warp;
-  griddep_wait();
-  const unsigned ep = __ldg(a.epoch);
-  if (p < a.lines) {
-    const size_t tile = (size_t)p * tl + t;
-    const size_t rec = a.shared || a.D ? (size_t)t : tile;
-    const double2 *F = a.F + rec * SQF;
-    double2 f0[SQE], f1[SQE];
-    double xr[SQE + 1];
-    {
-      const double *v = a.vin + (size_t)p * a.n;
-      const int t0 = t * SQT;
-#pragma unroll
-      for (int kk = 0; kk < SQE; ++kk) {
-        const int i = lane + 32 * kk;
-        xr[kk] = t0 + i < a.n ? __ldg(v + t0 + i) : 0.0;
-      }
-      xr[SQE] = lane == 0 && t0 + SQT < a.n ? __ldg(v + t0 + SQT) : 0.0;
-    }
-    if (a.D) {  // split records: shared ratios, the line's (delta, mu)
-      const double2 *D = a.D + tile * SQW;
-#pragma unroll
-      for (int k = 0; k < SQE; ++k) {
-        const double2 dk = __ldcs(D + k * 32 + lane);
-        f0[k] = make_double2(__ldg(&F[k * 32 + lane].x), dk.x);
-        f1[k] = make_double2(__ldg(&F[(SQE + k) * 32 + lane].x), dk.y);
-      }
-    } else if (a.shared) {
-#pragma unroll
-      for (int k = 0; k < SQE; ++k) {
-        f0[k] = __ldg(F + k * 32 + lane);
-        f1[k] = __ldg(F + (SQE + k) * 32 + lane);
-      }
-    } else if (role == 0) {  // (stays in L2 for the apply CTA)
-#pragma unroll
-      for (int k = 0; k < SQE; ++k) {
-        f0[k] = __ldcg(F + k * 32 + lane);
-        f1[k] = __ldcg(F + (SQE + k) * 32 + lane);
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < SQE; ++k) {
-        f0[k] = __ldcs(F + k * 32 + lane);
-        f1[k] = __ldcs(F + (SQE + k) * 32 + lane);
-      }
-    }
-    double x[SQE + 1];
-    double *sw = so[warp];
-#pragma unroll
-    for (int kk = 0; kk < SQE; ++kk) sw[sq_pad(lane + 32 * kk)] = xr[kk];
-    if (lane == 0) sw[sq_pad(SQT)] = xr[SQE];
-    __syncwarp();
-#pragma unroll
-    for (int kk = 0; kk <= SQE; ++kk) x[kk] = sw[sq_pad(SQE * lane + kk)];
-    __syncwarp();
-    // lane maps: forward P_end = af P_in + cf, backward Q_first = ab Q_after + cb
-    double af = 1.0, cf = 0.0, ab = 1.0, cb = 0.0;
-#pragma unroll
-    for (int k = 0; k < SQE; ++k) {
-      f0[k].y = __dmul_rn(f0[k].y, x[k]);      // delta v
-      f1[k].y = __dmul_rn(f1[k].y, x[k + 1]);  // mu v_{+1}
-      af = __dmul_rn(f0[k].x, af);
-      cf = __dadd_rn(__dmul_rn(f0[k].x, cf), f0[k].y);
-    }
-#pragma unroll
-    for (int k = SQE - 1; k >= 0; --k) {
-      ab = __dmul_rn(f1[k].x, ab);
-      cb = __dadd_rn(__dmul_rn(f1[k].x, cb), f1[k].y);
-    }
-    // inclusive scans of the lane maps (in-tile products stay in range: no guards)
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const double oa = __shfl_up_sync(0xffffffffu, af, off);
-      const double oc = __shfl_up_sync(0xffffffffu, cf, off);
-      const double ob = __shfl_down_sync(0xffffffffu, ab, off);
-      const double od = __shfl_down_sync(0xffffffffu, cb, off);
-      if (lane >= off) { cf = __fma_rn(af, oc, cf); af = __dmul_rn(af, oa); }
-      if (lane + off < 32) { cb = __fma_rn(ab, od, cb); ab = __dmul_rn(ab, ob); }
-    }
-    // the tile's maps: lane 31 holds the forward one, lane 0 the backward one
-    const double ma = __shfl_sync(0xffffffffu, af, 31), mc = __shfl_sync(0xffffffffu, cf, 31);
-    const double mb = __shfl_sync(0xffffffffu, ab, 0), md = __shfl_sync(0xffffffffu, cb, 0);
-    double *line = a.chain + 8 * (size_t)p * tl;
-    if (lane == 0 && role != 1) {  // publish: the maps, then the epoch (release)
-      double *mp = line + 8 * t;
-      __stcg(reinterpret_cast<double2 *>(mp), make_double2(ma, mc));
-      __stcg(reinterpret_cast<double2 *>(mp) + 1, make_double2(mb, md));
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(mp + 4), "r"(ep) : "memory");
-    }
-    if (role == 0) return;  // (a pre CTA: no barrier below is needed by anyone)
-    double exa = __shfl_up_sync(0xffffffffu, af, 1), exc = __shfl_up_sync(0xffffffffu, cf, 1);
-    double exb = __shfl_down_sync(0xffffffffu, ab, 1), exd = __shfl_down_sync(0xffffffffu, cb, 1);
-    if (lane == 0) { exa = 1.0; exc = 0.0; }
-    if (lane == 31) { exb = 1.0; exd = 0.0; }
-    // lane j: tile j's maps of this line (its own from registers)
-    double fa = 1.0, fc = 0.0, ba = 1.0, bc = 0.0;
-    if (lane == t) { fa = ma; fc = mc; ba = mb; bc = md; }
-    else if (lane < tl) {
-      const double *mp = line + 8 * lane;
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(mp + 4) : "memory");
-      } while (v != ep);
-      const double2 m0 = __ldcg(reinterpret_cast<const double2 *>(mp));
-      const double2 m1 = __ldcg(reinterpret_cast<const double2 *>(mp) + 1);
-      fa = m0.x; fc = m0.y; ba = m1.x; bc = m1.y;
-    }
-    __syncwarp();
-    // guarded inclusive scans along the line (cross-tile products may overflow
-    // or underflow: a structurally zero state stays zero, as tf_cat_g)
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const double oa = __shfl_up_sync(0xffffffffu, fa, off);
-      const double oc = __shfl_up_sync(0xffffffffu, fc, off);
-      const double ob = __shfl_down_sync(0xffffffffu, ba, off);
-      const double od = __shfl_down_sync(0xffffffffu, bc, off);
-      if (lane >= off) { fc = __dadd_rn(gm(fa, oc), fc); fa = gm(fa, oa); }
-      if (lane + off < 32) { bc = __dadd_rn(gm(ba, od), bc); ba = gm(ba, ob); }
-    }
-    // the tile's incoming states: P after tile t - 1, Q before tile t + 1 (zero at the line's ends)
-    double pin = __shfl_sync(0xffffffffu, fc, t > 0 ? t - 1 : 0);
-    double qin = __shfl_sync(0xffffffffu, bc, t + 1 < 32 ? t + 1 : 31);
-    if (t == 0) pin = 0.0;
-    if (t + 1 >= tl) qin = 0.0;
-    // this lane's incoming states, then the final recurrences
-    // (_kernels.py:65-67 / :80-87 order)
-    double pp = __dadd_rn(gm(exa, pin), exc), qq = __dadd_rn(gm(exb, qin), exd);
-#pragma unroll
-    for (int k = 0; k < SQE; ++k) {
-      pp = __dadd_rn(__dmul_rn(f0[k].x, pp), f0[k].y);
-      f0[k].y = pp;
-    }
-#pragma unroll
-    for (int k = SQE - 1; k >= 0; --k) {
-      qq = __dadd_rn(__dmul_rn(f1[k].x, qq), f1[k].y);
-      sw[SQE * lane + k] = __dadd_rn(f0[k].y, qq);
-    }
-  }
-  if (role == 0) return;
-  __syncthreads();
-  const int cnt = min(SQT, a.n - t * SQT);
-  if (!a.ew) {
-    for (int k = threadIdx.x; k < cnt * LPC; k += THR) {
-      const int i = k / LPC, w = k % LPC;
-      if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = so[w][i];
-    }
-    griddep_launch();
-    return;
-  }
-  // the grid's scaling update on the same addresses (k_sq_apply's)
-  double err = 0.0, vmax = 0.0, vmin = INFINITY;
-  long long fail = LLONG_MAX;
-  constexpr int EPER = SQT * LPC / THR;
-  double wq[EPER], sq[EPER];
-#pragma unroll
-  for (int q = 0; q < EPER; ++q) {
-    const int k = threadIdx.x + q * THR, i = k / LPC, w = k % LPC;
-    const bool live = k < cnt * LPC && p0 + w < a.lines;
-    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
-    wq[q] = live ? __ldcs(a.ew + idx) : 0.0;
-    sq[q] = live && a.eerr ? __ldcs(a.esc + idx) : 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < EPER; ++q) {
-    const int k = threadIdx.x + q * THR, i = k / LPC, w = k % LPC;
-    if (k >= cnt * LPC || p0 + w >= a.lines) continue;
-    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
-    const long long kg = a.ek0 + p0 + w + (long long)a.eng * (t * SQT + i);
-    const double wv = wq[q], tt = so[w][i];
-    if (a.eerr) err = __dadd_rn(err, fabs(__dsub_rn(__dmul_rn(sq[q], tt), wv)));
-    double nv;
-    if (tt == 0.0) {
-      if (wv > 0.0) fail = min(fail, (kg << 2) | ST_ZD);
-      nv = 0.0;
-    } else {
-      nv = __ddiv_rn(wv, tt);
-      if (!isfinite(nv)) fail = min(fail, (kg << 2) | ST_NF);
-      else if (wv > 0.0) {
-        vmax = fmax(vmax, nv);
-        vmin = fmin(vmin, nv);
-      }
-    }
-    a.esc[idx] = nv;
-  }
-  epi_block_part(err, vmax, vmin, fail, a.epart + (size_t)grp * tl + t);
   griddep_launch();
 }
 
