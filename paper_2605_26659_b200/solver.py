@@ -324,25 +324,50 @@ def _stage_stream(k):
 
 
 def _pipeline_ranges(sizes):
-    """Problem ranges of the batched API's pipeline stages: k = P // 2048
-    stages (at most 8) of >= 2048 problems and >= 2^22 points, one stage for
-    smaller batches; with FINOM_PIPE_FIRST set, a small first stage of that
-    many problems (the device starts sooner) before the k stages.
-    FINOM_PIPE_STAGES overrides k.  (Config 5, 8192 x 16384, warm calls: 1
-    stage 1.53 s; 8 stages of 1024 1.23-1.81 s -- each stage's loop takes 144
-    ms against 131 for 1/8 of the batch, and the host's preparation of a
-    1024-problem stage sometimes outlasts it; 4 stages of 2048 1.20-1.21 s,
-    each loop 265-279 ms.)"""
+    """Problem ranges of the batched API's pipeline stages.
+
+    Batches of >= 1024 problems and >= 2^24 points run as a short first and
+    last stage around equal middle stages of ~2368 problems: the first
+    stage's preparation (plan + host -> device) and the last stage's fetch are
+    the only transfers the device loops do not hide, so those two stages are
+    small -- 4 x 148 problems (two rounds of the 296 problems a B200 holds at
+    8 warps per problem) from 4096 problems on, 2 x 148 below -- and a second
+    stage of twice the first follows when the batch allows, so that every
+    stage's preparation hides behind the loop before it.  Smaller batches
+    take one stage.  FINOM_PIPE_SIZES = "n0,n1,..." sets the stages'
+    problem counts; FINOM_PIPE_STAGES = k asks for k equal stages
+    (FINOM_PIPE_FIRST: a small first stage of that many problems before them).
+    Config 5 (8192 x 16384, warm calls): 1 stage 1.53 s; 8 stages of 1024
+    1.23-1.81 s (each stage's loop takes 144 ms against 131 for 1/8 of the
+    batch, and the host's preparation of a stage sometimes outlasts it); 4
+    stages of 2048 1.07-1.08 s; 592 + 3 x 2336 + 592 1.02-1.03 s; 592 + 1184 +
+    2 x 2912 + 592 1.01 s for 0.97 s of device loops.  A rank's share of the
+    batch at 2 / 4 / 8 GPUs (4096 / 2048 / 1024 problems): 0.546 / 0.278 /
+    0.151 s against 0.588 / 0.355 / 0.197 s unstaged or in stages of 2048."""
     P, pts = len(sizes), int(np.sum(sizes))
-    k = min(8, P // 2048, pts >> 22)
+    explicit = os.environ.get("FINOM_PIPE_SIZES")
+    if explicit:
+        cuts = np.minimum(np.cumsum([0] + [int(t) for t in explicit.split(",")]), P)
+        cuts[-1] = P
+        return [(int(lo), int(hi)) for lo, hi in zip(cuts[:-1], cuts[1:]) if hi > lo]
     env = os.environ.get("FINOM_PIPE_STAGES")
     if env:
-        k = int(env)
-    k = max(1, min(k, P))
-    f = int(os.environ.get("FINOM_PIPE_FIRST", "0")) if k > 1 else 0
-    f = max(0, min(f, P - k))
-    return ([(0, f)] if f else []) + [(f + (P - f) * i // k, f + (P - f) * (i + 1) // k)
-                                      for i in range(k)]
+        k = max(1, min(int(env), P))
+        f = int(os.environ.get("FINOM_PIPE_FIRST", "0")) if k > 1 else 0
+        f = max(0, min(f, P - k))
+        return ([(0, f)] if f else []) + [(f + (P - f) * i // k, f + (P - f) * (i + 1) // k)
+                                          for i in range(k)]
+    if P < 1024 or pts < (1 << 24):
+        return [(0, P)]
+    edge = 4 * 148 if P >= 4096 else 2 * 148
+    # a second stage of twice the first when the batch allows: its preparation
+    # hides behind the first stage's loop, the big stages' behind its own
+    head = [edge, 2 * edge] if P - 4 * edge >= 2 * edge else [edge]
+    lo = sum(head)
+    mid = P - lo - edge
+    k = max(1, int(round(mid / 2368.0)))
+    cuts = [0] + list(np.cumsum(head)) + [lo + mid * (i + 1) // k for i in range(k)] + [P]
+    return [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])]
 
 
 def sinkhorn_1d_batched(xs, ys, us, vs, config, epsilons=None):

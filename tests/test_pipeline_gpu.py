@@ -21,9 +21,30 @@ def _batch(B, n):
 def test_stage_ranges():
     sizes = np.full(8192, 16384)
     r = S._pipeline_ranges(sizes)
-    assert len(r) == 4 and r[0] == (0, 2048) and r[-1] == (6144, 8192)
-    assert len(S._pipeline_ranges(np.full(2048, 16384))) == 1  # (a rank of a 4-way split)
+    # short first / last stages (two rounds of resident problems) around equal middle stages
+    assert r == [(0, 592), (592, 1776), (1776, 4688), (4688, 7600), (7600, 8192)]
+    r = S._pipeline_ranges(np.full(2048, 16384))  # (a rank of a 4-way split)
+    assert r == [(0, 296), (296, 888), (888, 1752), (1752, 2048)]
+    assert S._pipeline_ranges(np.full(1024, 16384)) == [(0, 296), (296, 728), (728, 1024)]
+    for P in (1024, 1500, 4096, 5000, 8192, 20000):  # contiguous, complete, non-empty
+        r = S._pipeline_ranges(np.full(P, 16384))
+        assert r[0][0] == 0 and r[-1][1] == P and all(lo < hi for lo, hi in r)
+        assert all(a[1] == b[0] for a, b in zip(r[:-1], r[1:]))
+    assert S._pipeline_ranges(np.full(1000, 16384)) == [(0, 1000)]
+    assert S._pipeline_ranges(np.full(2048, 1000)) == [(0, 2048)]  # (few points: one stage)
     assert S._pipeline_ranges(np.full(40, 1000)) == [(0, 40)]
+
+
+def test_stage_ranges_overrides(monkeypatch):
+    sizes = np.full(8192, 16384)
+    monkeypatch.setenv("FINOM_PIPE_STAGES", "4")
+    r = S._pipeline_ranges(sizes)
+    assert len(r) == 4 and r[0] == (0, 2048) and r[-1] == (6144, 8192)
+    monkeypatch.setenv("FINOM_PIPE_FIRST", "256")
+    r = S._pipeline_ranges(sizes)
+    assert len(r) == 5 and r[0] == (0, 256) and r[-1][1] == 8192
+    monkeypatch.setenv("FINOM_PIPE_SIZES", "100,200,300")
+    assert S._pipeline_ranges(sizes) == [(0, 100), (100, 300), (300, 8192)]
 
 
 @pytest.mark.gpu
