@@ -342,7 +342,7 @@ def _pipeline_ranges(sizes):
     batch, and the host's preparation of a stage sometimes outlasts it); 4
     stages of 2048 1.07-1.08 s; 592 + 3 x 2336 + 592 1.02-1.03 s; 592 + 1184 +
     2 x 2912 + 592 1.01 s for 0.97 s of device loops.  A rank's share of the
-    batch at 2 / 4 / 8 GPUs (4096 / 2048 / 1024 problems): 0.546 / 0.278 /
+    batch at 2 / 4 / 8 GPUs (4096 / 2048 / 1024 problems): 0.521 / 0.267 /
     0.151 s against 0.588 / 0.355 / 0.197 s unstaged or in stages of 2048."""
     P, pts = len(sizes), int(np.sum(sizes))
     explicit = os.environ.get("FINOM_PIPE_SIZES")

@@ -48,13 +48,18 @@ def test_stage_ranges_overrides(monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("stages", ["3", "5"])
+@pytest.mark.parametrize("stages", ["3", "5", "sizes:2,4,19,9,3"])
 def test_pipeline_matches_single_stage(monkeypatch, stages):
     xs, ys, us, vs, eps, probs = _batch(37, 1500)
     cfg = fb.SolverConfig(epsilon=1.0, itr_max=60, tol=0.0, stabilize=True, absorb_threshold=30.0)
     monkeypatch.setenv("FINOM_PIPE_STAGES", "1")
     one = fb.sinkhorn_1d_batched(xs, ys, us, vs, cfg, epsilons=eps)
-    monkeypatch.setenv("FINOM_PIPE_STAGES", stages)
+    if stages.startswith("sizes:"):  # short first / last stages (the default shape of large batches)
+        monkeypatch.delenv("FINOM_PIPE_STAGES")
+        monkeypatch.setenv("FINOM_PIPE_SIZES", stages[6:])
+        assert S._pipeline_ranges(np.full(37, 1500)) == [(0, 2), (2, 6), (6, 25), (25, 34), (34, 37)]
+    else:
+        monkeypatch.setenv("FINOM_PIPE_STAGES", stages)
     many = fb.sinkhorn_1d_batched(xs, ys, us, vs, cfg, epsilons=eps)
     assert np.array_equal(one.phi, many.phi) and np.array_equal(one.psi, many.psi)
     assert np.array_equal(one.a, many.a) and np.array_equal(one.b, many.b)
