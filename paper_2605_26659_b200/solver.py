@@ -334,7 +334,8 @@ def _pipeline_ranges(sizes):
     8 warps per problem) from 4096 problems on, 2 x 148 below -- and a second
     stage of twice the first follows when the batch allows, so that every
     stage's preparation hides behind the loop before it.  Smaller batches
-    take one stage.  FINOM_PIPE_SIZES = "n0,n1,..." sets the stages'
+    take one stage; batches of many small problems (< 4096 points each on
+    average) equal stages of >= 2048 problems and >= 2^22 points.  FINOM_PIPE_SIZES = "n0,n1,..." sets the stages'
     problem counts; FINOM_PIPE_STAGES = k asks for k equal stages
     (FINOM_PIPE_FIRST: a small first stage of that many problems before them).
     Config 5 (8192 x 16384, warm calls): 1 stage 1.53 s; 8 stages of 1024
@@ -359,6 +360,11 @@ def _pipeline_ranges(sizes):
                                           for i in range(k)]
     if P < 1024 or pts < (1 << 24):
         return [(0, P)]
+    if pts < 4096 * P:
+        # many small problems: equal stages of >= 2048 problems and >= 2^22
+        # points (the short stages above would be all overhead)
+        k = max(1, min(8, P // 2048, pts >> 22))
+        return [(P * i // k, P * (i + 1) // k) for i in range(k)]
     edge = 4 * 148 if P >= 4096 else 2 * 148
     # a second stage of twice the first when the batch allows: its preparation
     # hides behind the first stage's loop, the big stages' behind its own

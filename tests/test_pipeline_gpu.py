@@ -32,6 +32,8 @@ def test_stage_ranges():
         assert all(a[1] == b[0] for a, b in zip(r[:-1], r[1:]))
     assert S._pipeline_ranges(np.full(1000, 16384)) == [(0, 1000)]
     assert S._pipeline_ranges(np.full(2048, 1000)) == [(0, 2048)]  # (few points: one stage)
+    r = S._pipeline_ranges(np.full(100000, 200))  # (many small problems: equal stages)
+    assert len(r) == 4 and r[0] == (0, 25000) and r[-1] == (75000, 100000)
     assert S._pipeline_ranges(np.full(40, 1000)) == [(0, 40)]
 
 
