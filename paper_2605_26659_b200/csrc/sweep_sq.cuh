@@ -655,4 +655,219 @@ __global__ void __launch_bounds__(32 * LPC * SQ_FUSE) k_sq_fused(SqArgs a) {
   griddep_launch();
 }
 
+// The same short-line sweep with ONE scan per tile (the default): the lane
+// maps of both recurrences come from the factors the warp holds in registers,
+// their inclusive warp scans give the tile's maps (lane 31 / lane 0) -- no W
+// records, no separate tile-map pass --, the maps of a line's <= SQ_FUSE tiles
+// meet in shared memory, a guarded two-component scan gives the tile's
+// incoming P / Q, and every lane starts its recurrences from
+// (lanes before) o (tiles before) applied to zero.  The reference's per-point
+// operations ((r * p) + acc, p + q; _kernels.py:65-67 / :80-87) are
+// unchanged; the cross-lane compositions are reassociated differently from
+// k_sq_fused / the three kernels (1e-14 apart).  Fewer instructions and one
+// dependent phase less per tile: config 3 26.0 -> 23.6 ms per solve even
+// through a cluster launch (the experiment this came from), see DESIGN.md.
+template <int LPC>
+__global__ void __launch_bounds__(32 * LPC * SQ_FUSE) k_sq_fuse1(SqArgs a) {
+  extern __shared__ __align__(16) double fsm[];
+  constexpr int GT = 32 * LPC;  // threads per tile group
+  __shared__ EpiPart sp[SQ_FUSE][LPC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = warp / LPC, l = warp % LPC, tl = a.tl;
+  const int p0 = blockIdx.x * LPC, p = p0 + l;
+  double *so = fsm + (size_t)warp * SQX;
+  // (fwd A, fwd C, bwd A, bwd C) per (line, tile)
+  double4 *maps = reinterpret_cast<double4 *>(fsm + (size_t)LPC * tl * SQX);
+  const bool live = p < a.lines;
+  const size_t tile = (size_t)p * tl + t;
+  double2 f0[SQE], f1[SQE];
+  double exa = 1.0, exc = 0.0, exb = 1.0, exd = 0.0;  // the lanes before / after this one
+  griddep_wait();
+  if (live) {
+    const size_t rec = a.shared || a.D ? (size_t)t : tile;
+    const double2 *F = a.F + rec * SQF;
+    // the input first (its staging is the first dependent use), then the factors
+    double xr[SQE + 1];
+    {
+      const double *v = a.vin + (size_t)p * a.n;
+      const int t0 = t * SQT;
+#pragma unroll
+      for (int kk = 0; kk < SQE; ++kk) {
+        const int i = lane + 32 * kk;
+        xr[kk] = t0 + i < a.n ? __ldg(v + t0 + i) : 0.0;
+      }
+      xr[SQE] = lane == 0 && t0 + SQT < a.n ? __ldg(v + t0 + SQT) : 0.0;
+    }
+    if (a.D) {  // split records: shared ratios, the line's (delta, mu)
+      const double2 *D = a.D + tile * SQW;
+#pragma unroll
+      for (int k = 0; k < SQE; ++k) {
+        const double2 dk = __ldcs(D + k * 32 + lane);
+        f0[k] = make_double2(__ldg(&F[k * 32 + lane].x), dk.x);
+        f1[k] = make_double2(__ldg(&F[(SQE + k) * 32 + lane].x), dk.y);
+      }
+    } else if (a.shared) {
+#pragma unroll
+      for (int k = 0; k < SQE; ++k) {
+        f0[k] = __ldg(F + k * 32 + lane);
+        f1[k] = __ldg(F + (SQE + k) * 32 + lane);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < SQE; ++k) {
+        f0[k] = __ldcs(F + k * 32 + lane);
+        f1[k] = __ldcs(F + (SQE + k) * 32 + lane);
+      }
+    }
+    double x[SQE + 1];
+#pragma unroll
+    for (int kk = 0; kk < SQE; ++kk) so[sq_pad(lane + 32 * kk)] = xr[kk];
+    if (lane == 0) so[sq_pad(SQT)] = xr[SQE];
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk <= SQE; ++kk) x[kk] = so[sq_pad(SQE * lane + kk)];
+    __syncwarp();
+    // lane maps: forward P_end = af P_in + cf, backward Q_first = ab Q_after + cb
+    double af = 1.0, cf = 0.0, ab = 1.0, cb = 0.0;
+#pragma unroll
+    for (int k = 0; k < SQE; ++k) {
+      f0[k].y = __dmul_rn(f0[k].y, x[k]);      // delta v
+      f1[k].y = __dmul_rn(f1[k].y, x[k + 1]);  // mu v_{+1}
+      af = __dmul_rn(f0[k].x, af);
+      cf = __dadd_rn(__dmul_rn(f0[k].x, cf), f0[k].y);
+    }
+#pragma unroll
+    for (int k = SQE - 1; k >= 0; --k) {
+      ab = __dmul_rn(f1[k].x, ab);
+      cb = __dadd_rn(__dmul_rn(f1[k].x, cb), f1[k].y);
+    }
+    // inclusive scans of the lane maps (in-tile products stay in range: no guards)
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double oa = __shfl_up_sync(0xffffffffu, af, off);
+      const double oc = __shfl_up_sync(0xffffffffu, cf, off);
+      const double ob = __shfl_down_sync(0xffffffffu, ab, off);
+      const double od = __shfl_down_sync(0xffffffffu, cb, off);
+      if (lane >= off) { cf = __fma_rn(af, oc, cf); af = __dmul_rn(af, oa); }
+      if (lane + off < 32) { cb = __fma_rn(ab, od, cb); ab = __dmul_rn(ab, ob); }
+    }
+    // the tile's maps: lane 31 holds the forward one, lane 0 the backward one
+    double *mp = reinterpret_cast<double *>(&maps[l * tl + t]);
+    if (lane == 31) { mp[0] = af; mp[1] = cf; }
+    if (lane == 0) { mp[2] = ab; mp[3] = cb; }
+    exa = __shfl_up_sync(0xffffffffu, af, 1);
+    exc = __shfl_up_sync(0xffffffffu, cf, 1);
+    exb = __shfl_down_sync(0xffffffffu, ab, 1);
+    exd = __shfl_down_sync(0xffffffffu, cb, 1);
+    if (lane == 0) { exa = 1.0; exc = 0.0; }
+    if (lane == 31) { exb = 1.0; exd = 0.0; }
+  }
+  __syncthreads();  // every tile map of the CTA's lines is written
+  if (live) {
+    // lane j: tile j's maps of this line; guarded inclusive scans along the
+    // line (cross-tile products may overflow or underflow: a structurally
+    // zero state stays zero, as tf_cat_g); SQ_FUSE <= 4 tiles: two levels
+    double fa = 1.0, fc = 0.0, ba = 1.0, bc = 0.0;
+    if (lane < tl) {
+      const double4 m = maps[l * tl + lane];
+      fa = m.x; fc = m.y; ba = m.z; bc = m.w;
+    }
+#pragma unroll
+    for (int off = 1; off < SQ_FUSE; off <<= 1) {
+      const double oa = __shfl_up_sync(0xffffffffu, fa, off);
+      const double oc = __shfl_up_sync(0xffffffffu, fc, off);
+      const double ob = __shfl_down_sync(0xffffffffu, ba, off);
+      const double od = __shfl_down_sync(0xffffffffu, bc, off);
+      if (lane >= off) { fc = __dadd_rn(gm(fa, oc), fc); fa = gm(fa, oa); }
+      if (lane + off < 32) { bc = __dadd_rn(gm(ba, od), bc); ba = gm(ba, ob); }
+    }
+    // the tile's incoming states: P after tile t - 1, Q before tile t + 1 (zero at the line's ends)
+    double pin = __shfl_sync(0xffffffffu, fc, t > 0 ? t - 1 : 0);
+    double qin = __shfl_sync(0xffffffffu, bc, t + 1);
+    if (t == 0) pin = 0.0;
+    if (t + 1 >= tl) qin = 0.0;
+    // this lane's incoming states, then the final recurrences
+    double pp = __dadd_rn(gm(exa, pin), exc), qq = __dadd_rn(gm(exb, qin), exd);
+#pragma unroll
+    for (int k = 0; k < SQE; ++k) {
+      pp = __dadd_rn(__dmul_rn(f0[k].x, pp), f0[k].y);
+      f0[k].y = pp;
+    }
+#pragma unroll
+    for (int k = SQE - 1; k >= 0; --k) {
+      qq = __dadd_rn(__dmul_rn(f1[k].x, qq), f1[k].y);
+      so[SQE * lane + k] = __dadd_rn(f0[k].y, qq);
+    }
+  }
+  // ---- per tile: transposed write or the fused scaling update (k_sq_apply's)
+  const int tid = threadIdx.x - GT * t;  // thread within the tile's group
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + t), "r"(GT) : "memory");
+  const int cnt = min(SQT, a.n - t * SQT);
+  double *sg = fsm + (size_t)t * LPC * SQX;  // the group's LPC output rows
+  if (!a.ew) {
+    for (int k = tid; k < cnt * LPC; k += GT) {
+      const int i = k / LPC, w = k % LPC;
+      if (p0 + w < a.lines) a.out_t[(size_t)(t * SQT + i) * a.lines + p0 + w] = sg[w * SQX + i];
+    }
+    griddep_launch();
+    return;
+  }
+  double err = 0.0, vmax = 0.0, vmin = INFINITY;
+  long long fail = LLONG_MAX;
+  constexpr int EPER = SQT * LPC / GT;
+  double wq[EPER], sq[EPER];
+#pragma unroll
+  for (int q = 0; q < EPER; ++q) {
+    const int k = tid + q * GT, i = k / LPC, w = k % LPC;
+    const bool lv = k < cnt * LPC && p0 + w < a.lines;
+    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+    wq[q] = lv ? __ldcs(a.ew + idx) : 0.0;
+    sq[q] = lv && a.eerr ? __ldcs(a.esc + idx) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < EPER; ++q) {
+    const int k = tid + q * GT, i = k / LPC, w = k % LPC;
+    if (k >= cnt * LPC || p0 + w >= a.lines) continue;
+    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+    const long long kg = a.ek0 + p0 + w + (long long)a.eng * (t * SQT + i);
+    const double wv = wq[q], tt = sg[w * SQX + i];
+    if (a.eerr) err = __dadd_rn(err, fabs(__dsub_rn(__dmul_rn(sq[q], tt), wv)));
+    double nv;
+    if (tt == 0.0) {
+      if (wv > 0.0) fail = min(fail, (kg << 2) | ST_ZD);
+      nv = 0.0;
+    } else {
+      nv = __ddiv_rn(wv, tt);
+      if (!isfinite(nv)) fail = min(fail, (kg << 2) | ST_NF);
+      else if (wv > 0.0) {
+        vmax = fmax(vmax, nv);
+        vmin = fmin(vmin, nv);
+      }
+    }
+    a.esc[idx] = nv;
+  }
+  // epi_block_part over the group's LPC warps (same fold order as a LPC-warp CTA)
+  err = warp_sum(err);
+  vmax = warp_max(vmax);
+  vmin = warp_min(vmin);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const long long o = __shfl_xor_sync(0xffffffffu, fail, off);
+    fail = o < fail ? o : fail;
+  }
+  if (lane == 0) sp[t][l] = EpiPart{err, vmax, vmin, fail};
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + t), "r"(GT) : "memory");
+  if (tid == 0) {
+    EpiPart r{0.0, 0.0, INFINITY, LLONG_MAX};
+    for (int w = 0; w < LPC; ++w) {
+      r.err += sp[t][w].err;
+      r.vmax = fmax(r.vmax, sp[t][w].vmax);
+      r.vmin = fmin(r.vmin, sp[t][w].vmin);
+      r.fail = sp[t][w].fail < r.fail ? sp[t][w].fail : r.fail;
+    }
+    a.epart[(size_t)blockIdx.x * tl + t] = r;
+  }
+  griddep_launch();
+}
+
 }  // namespace fb

@@ -190,13 +190,15 @@ def test_row_sharded_2d_nccl_world1():
 
 @pytest.mark.parametrize("env,n", [({"FB_GRAPH2D": "0"}, 96), ({"FB_SQ_SPLIT": "0"}, 96),
                                    ({"FB_SQ": "0"}, 96), ({"FB_SQ_FUSE": "0"}, 96),
-                                   ({"FB_SQ_FUSE": "0"}, 700)])
+                                   ({"FB_SQ_FUSE": "0"}, 700), ({"FB_SQ_FUSE": "2"}, 96),
+                                   ({"FB_SQ_FUSE": "2"}, 700), ({"FB_SQ_FUSE": "2"}, 1024)])
 def test_2d_loop_variants_agree(monkeypatch, env, n):
-    """The device-looped graph vs the host-stepped loop and the fused short-line
-    sweep vs its three kernels (bitwise: the same operations), split vs full
-    square-sweep records and square vs general sweeps (1e-12): absorbed
-    config-3-style grid with a zero-mass stretch and a tol stop (n = 700:
-    three ragged tiles per line)."""
+    """The device-looped graph vs the host-stepped loop (bitwise: the same
+    operations); the one-scan fused short-line sweep (default) vs the three
+    kernels and vs the two-scan fused sweep, split vs full square-sweep
+    records and square vs general sweeps (1e-12): absorbed config-3-style grid
+    with a zero-mass stretch and a tol stop (n = 700: three ragged tiles per
+    line; 1024: four full tiles)."""
     x1, y1, x2, y2, U, V, eps = W.config3(n=n)
     U = U.copy()
     U[10:30, 40:50] = 0.0
@@ -210,9 +212,25 @@ def test_2d_loop_variants_agree(monkeypatch, env, n):
     assert base.iterations_run == alt.iterations_run and base.converged == alt.converged
     assert list(base.absorb_iterations) == list(alt.absorb_iterations)
     assert len(base.absorb_iterations) >= 1
-    tol = 0.0 if "FB_GRAPH2D" in env or "FB_SQ_FUSE" in env else 1e-12
+    tol = 0.0 if "FB_GRAPH2D" in env else 1e-12
     assert rel_inf(alt.phi, base.phi) <= tol and rel_inf(alt.psi, base.psi) <= tol
     assert abs(alt.cost - base.cost) <= max(tol, 1e-15) * abs(base.cost)
+
+
+@pytest.mark.parametrize("n", [96, 700])
+def test_two_scan_fused_sweep_is_the_three_kernels(monkeypatch, n):
+    """k_sq_fused (FB_SQ_FUSE=2) runs the three kernels' operations in their
+    order: bitwise equal results."""
+    x1, y1, x2, y2, U, V, eps = W.config3(n=n)
+    cfg = fb.SolverConfig(epsilon=eps, itr_max=40, tol=0.0, stabilize=True, absorb_threshold=6.0)
+    args = (_grid(x1, y1), _grid(x2, y2), fb.Measure2D(U), fb.Measure2D(V), cfg)
+    monkeypatch.setenv("FB_SQ_FUSE", "2")
+    two = fb.sinkhorn_2d(*args)
+    monkeypatch.setenv("FB_SQ_FUSE", "0")
+    three = fb.sinkhorn_2d(*args)
+    assert list(two.absorb_iterations) == list(three.absorb_iterations)
+    assert np.array_equal(two.phi, three.phi) and np.array_equal(two.psi, three.psi)
+    assert two.cost == three.cost
 
 
 @pytest.mark.parametrize("graph", ["1", "0"])
