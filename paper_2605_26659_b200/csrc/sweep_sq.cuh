@@ -231,6 +231,8 @@ __global__ void __launch_bounds__(NTHR) k_sq_pre(SqArgs a) {
   const double2 *D = a.D ? a.D + (size_t)w * SQW : nullptr;
   __shared__ double xs[WPC][SQX];
   double x[SQE + 1];
+  double2 sprod = make_double2(1.0, 1.0);  // (lane 0: the tile's ratio products, loaded early)
+  if (lane == 0) sprod = __ldg(a.S + rec);
   sq_load_v(a.vin + (size_t)p * a.n, t * SQT, a.n, xs[threadIdx.x >> 5], x);
   double cf = 0.0, cb = 0.0;
 #pragma unroll
@@ -246,10 +248,9 @@ __global__ void __launch_bounds__(NTHR) k_sq_pre(SqArgs a) {
   cf = warp_sum(cf);
   cb = warp_sum(cb);
   if (lane == 0) {
-    const double2 s = __ldg(a.S + rec);
     Node *nd = a.nodes + w;
-    nd->tf = Tf{s.x, 0.0, cf, 1.0, 0.0};
-    nd->tb = Tf{s.y, 0.0, cb, 1.0, 0.0};
+    nd->tf = Tf{sprod.x, 0.0, cf, 1.0, 0.0};
+    nd->tb = Tf{sprod.y, 0.0, cb, 1.0, 0.0};
   }
   griddep_launch();
 }
@@ -341,6 +342,15 @@ __global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
     const size_t rec = a.shared || a.D ? (size_t)t : tile;
     const double2 *F = a.F + rec * SQF;
     double2 f0[SQE], f1[SQE];
+    // lanes 0 / 31: the tile's exclusive maps and the line's incoming carry
+    // (their latency hides behind the loads below)
+    double nA = 1.0, nC = 0.0, ncar = 0.0;
+    if (lane == 0 || lane == 31) {
+      const Tf *xm = lane == 0 ? &a.nodes[tile].xf : &a.nodes[tile].xb;
+      nA = __ldcg(&xm->A);
+      nC = __ldcg(&xm->C);
+      if (a.carry) ncar = __ldg(a.carry + 4 * (size_t)p + (lane == 0 ? 0 : 2));
+    }
     // the input first (its staging is the first dependent use), then the
     // factors (config 4: 437 -> 423 ms per solve)
     double xr[SQE + 1];
@@ -383,14 +393,8 @@ __global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
     double pin = 0.0, qin = 0.0;  // the tile's incoming P (lane 0) / Q (lane 31)
     // (the tile's exclusive maps applied to the line's incoming states: zero,
     // or a row shard's carries from the other shards, as tf_apply_g)
-    if (lane == 0) {
-      const double cp = a.carry ? __ldg(a.carry + 4 * (size_t)p) : 0.0;
-      pin = (gm(__ldcg(&a.nodes[tile].xf.A), cp) + 0.0) + __ldcg(&a.nodes[tile].xf.C);
-    }
-    if (lane == 31) {
-      const double cq = a.carry ? __ldg(a.carry + 4 * (size_t)p + 2) : 0.0;
-      qin = (gm(__ldcg(&a.nodes[tile].xb.A), cq) + 0.0) + __ldcg(&a.nodes[tile].xb.C);
-    }
+    if (lane == 0) pin = (gm(nA, ncar) + 0.0) + nC;
+    if (lane == 31) qin = (gm(nA, ncar) + 0.0) + nC;
     // lane maps: forward P_end = af P_in + cf, backward Q_first = ab Q_after + cb
     double af = 1.0, cf = 0.0, ab = 1.0, cb = 0.0;
 #pragma unroll
