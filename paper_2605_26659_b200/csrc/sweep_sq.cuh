@@ -337,6 +337,25 @@ __global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x % a.tl, p0 = (blockIdx.x / a.tl) * LPC, p = p0 + warp;
   griddep_wait();
+  // the fused scaling update's operands (weights, old scalings) start into
+  // shared memory with the tile's other loads (cp.async: no registers held),
+  // each thread its own elements: the update finds them on chip instead of
+  // paying a second DRAM round trip at the end of the CTA (config 4: 399 ->
+  // 381 ms per solve; 4 lines per CTA only -- 16 KB of shared memory)
+  __shared__ double sew[LPC == 4 ? 2 * LPC * SQT : 1];
+  if (LPC == 4 && a.ew) {
+    const int cnt0 = min(SQT, a.n - t * SQT);
+#pragma unroll
+    for (int q = 0; q < SQT * LPC / THR; ++q) {
+      const int kk = threadIdx.x + q * THR, i = kk / LPC, w = kk % LPC;
+      if (kk < cnt0 * LPC && p0 + w < a.lines) {
+        const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+        cp_async8(sew + kk, a.ew + idx);
+        if (a.eerr) cp_async8(sew + LPC * SQT + kk, a.esc + idx);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   if (p < a.lines) {
     const size_t tile = (size_t)p * a.tl + t;
     const size_t rec = a.shared || a.D ? (size_t)t : tile;
@@ -453,13 +472,24 @@ __global__ void __launch_bounds__(32 * LPC) k_sq_apply(SqArgs a) {
   // every load of the thread's elements is issued before the first use
   constexpr int EPER = SQT * LPC / THR;
   double wq[EPER], sq[EPER];
+  if (LPC == 4) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
-  for (int q = 0; q < EPER; ++q) {
-    const int k = threadIdx.x + q * THR, i = k / LPC, w = k % LPC;
-    const bool live = k < cnt * LPC && p0 + w < a.lines;
-    const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
-    wq[q] = live ? __ldcs(a.ew + idx) : 0.0;
-    sq[q] = live && a.eerr ? __ldcs(a.esc + idx) : 0.0;
+    for (int q = 0; q < EPER; ++q) {
+      const int k = threadIdx.x + q * THR, w = k % LPC;
+      const bool live = k < cnt * LPC && p0 + w < a.lines;
+      wq[q] = live ? sew[k] : 0.0;
+      sq[q] = live && a.eerr ? sew[LPC * SQT + k] : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < EPER; ++q) {
+      const int k = threadIdx.x + q * THR, i = k / LPC, w = k % LPC;
+      const bool live = k < cnt * LPC && p0 + w < a.lines;
+      const long long idx = (long long)(t * SQT + i) * a.lines + p0 + w;
+      wq[q] = live ? __ldcs(a.ew + idx) : 0.0;
+      sq[q] = live && a.eerr ? __ldcs(a.esc + idx) : 0.0;
+    }
   }
 #pragma unroll
   for (int q = 0; q < EPER; ++q) {
